@@ -1,0 +1,375 @@
+#!/usr/bin/env python3
+"""Benchmark of the fp64 PIC step (BASELINE.json metric: particle updates/s,
+ns/particle/step, % HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
+                    [--impl ours|reference] [--no-e2e] [--no-cpu-baseline]
+
+A "step" is one PIC time step of the whole hot path (SURVEY.md sec. 8a:
+sort every K steps, fused gather/push/deposit, J fold, Yee update) over the
+workload's synthetic particles.  At N=1 the default workload is C2 =
+BASELINE.json configs[1] (40^3, 50 e/cell = 3.2M particles; its particle
+state, 180 MB, is larger than the 126 MB L2, so no explicit L2 flush).
+
+--impl reference times the CPU oracle (oracle/, plain serial C) on the same
+workload: each step pushes a fixed bounded sample of the particles through
+one oracle step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle updates/sec (ns/particle/step), fp64, 1/2/4/8 B200; % HBM roofline"
+UNIT = "particle-updates/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML every ~5 ms."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv = None
+            self.err = str(e)
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def pinned_copy(P, ids):
+    import torch
+    tp = torch.empty(P.shape, dtype=torch.float64, pin_memory=True)
+    tp.numpy()[:] = P
+    ti = torch.empty(ids.shape, dtype=torch.int64, pin_memory=True)
+    ti.numpy().view(np.uint64)[:] = ids
+    return tp, ti, tp.numpy(), ti.numpy().view(np.uint64)
+
+
+def oracle_sample_rate(wl, parts, target_s=10.0, max_particles=None):
+    """Time the oracle as it stands (single thread) on a bounded sample:
+    full oracle steps of the workload when one fits in target_s, else a
+    contiguous particle sample pushed through one oracle step."""
+    from oracle import oracle as O
+    O.build()
+    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every)
+    sub = []
+    n_tot = sum(p.shape[1] for p, _ in parts)
+    frac = 1.0 if max_particles is None else min(1.0, max_particles / n_tot)
+    for P, ids in parts:
+        k = max(1, int(P.shape[1] * frac))
+        sub.append((P[:, :k].copy(), ids[:k].copy()))
+    orc = O.Oracle(g, particles=sub)
+    n_sample = sum(p.shape[1] for p, _ in sub)
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        orc.step(1)
+        steps += 1
+        if time.perf_counter() - t0 >= target_s:
+            break
+    dt = time.perf_counter() - t0
+    return n_sample * steps / dt, n_sample, steps, dt
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return
+    from synth import gen_particles
+    parts = gen_particles(wl)
+    from oracle import oracle as O
+    O.build()
+    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every)
+    n_sample = args.ref_sample
+    sub = []
+    for P, ids in parts:
+        k = min(P.shape[1], max(1, n_sample // len(parts)))
+        sub.append((P[:, :k].copy(), ids[:k].copy()))
+    orc = O.Oracle(g, particles=sub)
+    ns = sum(p.shape[1] for p, _ in sub)
+    for _ in range(args.warmup):
+        orc.step(1)
+    t0 = time.perf_counter()
+    orc.step(args.steps)
+    dt = time.perf_counter() - t0
+    v = ns * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "ns_per_particle_step": 1e9 / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": wl_config(wl, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {ns} particles of {wl.name} (of {wl.n_particles}) "
+                                   f"through full oracle steps (fields on the whole grid), "
+                                   f"single thread"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def wl_config(wl, world):
+    return {"workload": wl.name, "grid": [wl.nx, wl.ny, wl.nz],
+            "particles": wl.n_particles, "species": len(wl.species),
+            "ppc": sum(s.ppc for s in wl.species), "sort_every": wl.sort_every,
+            "supercell": wl.supercell, "dt": wl.dt,
+            "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (particle state > 126 MB), no flush"}
+
+
+def run_ours(args, wl, rank, world, local):
+    import torch
+
+    import paper_1608_01009_b200 as pkg
+    from synth import gen_particles
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    parts = gen_particles(wl, rank=rank if world > 1 else None)
+    n_local = sum(p.shape[1] for p, _ in parts)
+
+    def new_sim(flags=0):
+        sim = pkg.simulation_from_workload(wl, capacity_factor=1.0, flags=flags,
+                                           rank=rank, nranks=world)
+        return sim
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---------------- device-resident timed region (value)
+    sim = new_sim()
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    sim.step(args.warmup)
+    sim.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(sim.stream)
+        sim.step(args.steps)
+        e1.record(sim.stream)
+        torch.cuda.synchronize()
+        barrier()
+    t_ms = e0.elapsed_time(e1)
+    launches = sim.launch_count()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        nt = torch.tensor([n_local], device="cuda", dtype=torch.float64)
+        dist.all_reduce(nt)
+        n_total = float(nt.item())
+    else:
+        n_total = float(n_local)
+    value = n_total * args.steps / (t_ms * 1e-3)
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+
+    # ---------------- profiled pass: per-stage CUDA events around each launch
+    psim = new_sim(pkg.FLAG_PROFILE)
+    for s, (P, ids) in enumerate(parts):
+        psim.set_particles(s, P, ids)
+    psim.step(args.warmup)
+    psim.stage_times()
+    psim.step(args.steps)
+    st = psim.stage_times()
+    psim.close()
+    del psim
+    torch.cuda.empty_cache()
+    ppc_cells = wl.nx * wl.ny * (wl.nz // world)
+    alg_bytes_total = sum(p.shape[1] for p, _ in parts) * 96.0 + len(parts) * ppc_cells * 72.0
+    n_launch = max(st["particle_launches"], 1)
+    per_launch_ms = st["particle"] / n_launch
+    per_launch_bytes = alg_bytes_total / len(parts)
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_particle_traffic.json")
+    if os.path.exists(tp):
+        try:
+            d = json.load(open(tp))
+            if d.get("workload") == wl.name:
+                traffic = d.get("bytes_per_launch")
+        except Exception:
+            pass
+    step_ms_prof = (st["sort"] + st["particle"] + st["field"] + st["exchange"]) / args.steps
+
+    # ---------------- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = [pinned_copy(P, ids) for P, ids in parts]
+        outs = [(np.empty_like(P), np.empty_like(ids)) for P, ids in parts]
+        esim = new_sim()
+        for s, (_, _, Pn, In) in enumerate(pinned):
+            esim.set_particles(s, Pn, In)
+        esim.step(args.warmup)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s, (_, _, Pn, In) in enumerate(pinned):
+            esim.set_particles(s, Pn, In)
+        esim.step(args.steps)
+        for s in range(len(parts)):
+            esim.get_particles(s, out=outs[s])
+        torch.cuda.synchronize()
+        barrier()
+        te = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        esim.close()
+        bytes_io = n_local * 56.0
+        e2e = {"value": n_total * args.steps / te, "unit": UNIT,
+               "h2d_bytes_per_step": bytes_io / args.steps, "d2h_bytes_per_step": bytes_io / args.steps,
+               "mode": "pinned host -> pic_set_particles (incl. sort) -> pic_step(K) -> "
+                       "pic_get_particles -> host, wall clock, max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, ns, nsteps, dt = oracle_sample_rate(wl, parts, target_s=args.cpu_seconds,
+                                               max_particles=args.cpu_max_particles)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{nsteps} oracle step(s) over {ns} of {wl.n_particles} particles of "
+                         f"{wl.name} (whole grid), {dt:.1f} s, single thread"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "ns_per_particle_step": 1e9 / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded numpy PCG64, DESIGN.md sec. 6)",
+            "config": wl_config(wl, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "particle (gather+Boris+VB deposit)",
+                         "alg_bytes_per_launch": per_launch_bytes,
+                         "avg_launch_ms": per_launch_ms, "peak_source": peak_src,
+                         "timing": "CUDA events around every particle-kernel launch on the "
+                                   "library stream, profiled pass of the same K steps",
+                         "step_share": st["particle"] / max(1e-9, step_ms_prof * args.steps),
+                         "stage_ms_per_step": {k: st[k] / args.steps for k in
+                                               ("sort", "particle", "field", "exchange")},
+                         "whole_step_frac": (alg_bytes_total + n_local * 112.0 / max(wl.sort_every, 1))
+                         / (t_ms * 1e-3 / args.steps) / 1e9 / peak},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-max-particles", type=int, default=None)
+    ap.add_argument("--ref-sample", type=int, default=50_000)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
+    rank, world, local = dist_env()
+    from synth import get_config
+    name = args.workload or ("C2" if world == 1 else "C4")
+    wl = get_config(name).for_ranks(world)
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+    else:
+        run_ours(args, wl, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/*
+ * pic.h -- C ABI of libpic.so, the B200-native fp64 particle-in-cell step.
+ *
+ * The operation (sec. 2, lines 36-40): macro-particles with charge
+ * q, mass m and weight w move under the relativistic equations of motion in
+ * the Yee-grid electromagnetic field; "the field is interpolated to the
+ * position of particles, while the contribution of each particle to the
+ * current density is distributed among the nearest grid nodes"; the stages
+ * are "numerical integration of Maxwell's equations, field interpolation,
+ * solving particles' equations of motion, and computing the current density".
+ * PAPER.md:48 fixes double precision, the cloud-in-cell form factor and the
+ * Villasenor-Buneman charge-conserving deposit.  The concrete scheme is
+ * SURVEY.md sec. 8a rows a1-a8 with the readings R1-R20 of DESIGN.md sec. 3.
+ *
+ * Units (R3): Gaussian, dB/dt = -c curl E, dE/dt = c curl B - 4 pi J;
+ * momenta are u = p/(m c) = gamma*beta.  Positions are physical
+ * coordinates in [0, L) with L = n * d per axis, periodic in x, y and z.
+ *
+ * Conventions for every call:
+ *  - returns PIC_OK (0) or a negative PIC_E* code; no exception, abort or
+ *    exit crosses the ABI.  pic_strerror(code) and pic_last_error(ctx) give
+ *    a message.
+ *  - host arrays are caller-owned; the library copies in / out and never
+ *    keeps a caller pointer.
+ *  - device memory is ONE caller-supplied workspace (d_workspace, `bytes`
+ *    long, 256-byte aligned) that must outlive the context; size it with
+ *    pic_workspace_size.  The library never calls cudaMalloc for state.
+ *  - all work is enqueued on cfg->stream (a cudaStream_t, NULL = legacy
+ *    default stream).  A context is used by one host thread at a time.
+ *  - nranks > 1 (z-slab decomposition) makes pic_init,
+ *    pic_step and pic_destroy collective over the ranks.
+ *
+ * There is no CPU fallback: without a CUDA device every call that touches
+ * the device returns PIC_ECUDA.
+ */
+#ifndef PIC_H
+#define PIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIC_MAX_SPECIES 4
+
+enum {
+    PIC_OK = 0,
+    PIC_EINVAL = -1,        /* bad config / argument (CFL, S not dividing extents, ...) */
+    PIC_ENOMEM = -2,        /* workspace too small */
+    PIC_ECAPACITY = -3,     /* particle capacity or caller buffer too small */
+    PIC_ESTATE = -4,        /* call order (e.g. step before init) */
+    PIC_EDISPLACEMENT = -5, /* some particle moved >= 1 cell on an axis in one step */
+    PIC_ENONFINITE = -6,    /* non-finite position or momentum */
+    PIC_ECUDA = -7,         /* CUDA runtime / driver failure (incl. no device) */
+    PIC_ENCCL = -8          /* NCCL failure (nranks > 1) */
+};
+
+/* All scalar fields are 8 bytes wide so the layout has no padding. */
+typedef struct pic_config {
+    int64_t nx, ny, nz;                /* GLOBAL cell counts */
+    double dx, dy, dz;                 /* cell size */
+    double dt, c;                      /* time step (must satisfy CFL), speed of light */
+    int64_t n_species;                 /* 1..PIC_MAX_SPECIES */
+    double q[PIC_MAX_SPECIES];         /* charge per species (units of e) */
+    double m[PIC_MAX_SPECIES];         /* mass per species (units of m_e) */
+    double w[PIC_MAX_SPECIES];         /* weight = real particles per macro-particle */
+    int64_t capacity[PIC_MAX_SPECIES]; /* max particles held by this rank, per species */
+    int64_t supercell;                 /* S: supercell edge (cells); must divide nx, ny, local nz */
+    int64_t sort_every;                /* K: re-sort at the start of step n when n % K == 0 (0: never) */
+    int64_t rank, nranks;              /* z-slab rank / count (1 for a single GPU) */
+    int64_t flags;                     /* PIC_FLAG_* bits */
+    uint8_t nccl_id[128];              /* ncclUniqueId from rank 0 (nranks > 1) */
+    void *stream;                      /* cudaStream_t all work is enqueued on */
+} pic_config;
+
+#define PIC_FLAG_NO_GRAPH 1   /* launch kernels directly instead of CUDA graphs */
+#define PIC_FLAG_PROFILE 2    /* record per-stage CUDA events (pic_get_stage_times) */
+#define PIC_FLAG_NAIVE 4      /* use the naive one-thread-per-particle kernel (tests) */
+
+typedef struct pic_ctx pic_ctx;
+
+/* Pure: device bytes pic_init needs for cfg (fields with ghost layers,
+ * double-buffered SoA particles with ids, sort scratch, offsets, error word).
+ * Returns PIC_EINVAL for an invalid cfg. */
+int pic_workspace_size(const pic_config *cfg, size_t *bytes);
+
+/* Validates cfg (dt <= 1/(c sqrt(1/dx^2+1/dy^2+1/dz^2)); S divides nx, ny and
+ * nz/nranks; 1 <= n_species <= PIC_MAX_SPECIES; m > 0), carves d_workspace
+ * (device pointer, `bytes` long), sets up NCCL when nranks > 1 and zeroes
+ * E, B, J and all particle counts.  The rank owns z in [rank*nz/nranks,
+ * (rank+1)*nz/nranks).  *out receives the context. */
+int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **out);
+
+/* Copies n particles of `species` from HOST arrays (global physical
+ * coordinates in [0,L), momenta u^{n-1/2}, 64-bit ids), keeps those whose
+ * z lies in this rank's slab, and sorts them.  Replaces the
+ * species' previous particles.  PIC_ECAPACITY if they exceed capacity;
+ * PIC_EINVAL for a position outside [0,L) or a bad species index. */
+int pic_set_particles(pic_ctx *ctx, int species, int64_t n,
+                      const double *x, const double *y, const double *z,
+                      const double *ux, const double *uy, const double *uz,
+                      const uint64_t *id);
+
+/* Copies E^n, B^n from a HOST array f[6][nz_local][ny][nx] (x fastest;
+ * order Ex,Ey,Ez,Bx,By,Bz; Yee-staggered as in DESIGN.md sec. 4). */
+int pic_set_fields(pic_ctx *ctx, const double *f);
+
+/* Advances nsteps time steps (per step: a1 sort when
+ * step % K == 0; a2-a6 fused gather/push/deposit per species; a7 Yee
+ * update; a8 exchange when nranks > 1).  Synchronises cfg->stream at the
+ * end and returns the sticky device error (PIC_EDISPLACEMENT,
+ * PIC_ENONFINITE, PIC_ECAPACITY) if one was raised. */
+int pic_step(pic_ctx *ctx, int64_t nsteps);
+
+/* Copies E^n, B^n and J^{n-1/2} (the last deposit; zero before the first
+ * step) of the local slab without ghosts into a HOST array
+ * f[9][nz_local][ny][nx] (Ex,Ey,Ez,Bx,By,Bz,Jx,Jy,Jz). */
+int pic_get_fields(pic_ctx *ctx, double *f);
+
+/* Copies the particles of `species` in their current (sorted) device order
+ * to HOST arrays.  *n_inout: capacity of the arrays in, particle count out
+ * (PIC_ECAPACITY, with the count written, when too small).  Positions are
+ * wrapped into [0,L).  Any array pointer may be NULL to skip it. */
+int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout,
+                      double *x, double *y, double *z,
+                      double *ux, double *uy, double *uz, uint64_t *id);
+
+/* Current particle count of a species on this rank. */
+int pic_get_count(pic_ctx *ctx, int species, int64_t *n);
+
+/* The step index n of the state (number of steps taken since pic_init). */
+int pic_get_step_index(pic_ctx *ctx, int64_t *n);
+
+/* With PIC_FLAG_PROFILE: accumulated device milliseconds per stage since
+ * the last call (ms[0] sort, ms[1] particle kernel, ms[2] field update,
+ * ms[3] exchange) and the number of particle-kernel launches; resets them. */
+int pic_get_stage_times(pic_ctx *ctx, double ms[4], int64_t *particle_launches);
+
+/* Number of kernel launches the library enqueued since the last call
+ * (counted on the host at enqueue time, graph nodes included); resets it. */
+int pic_get_launch_count(pic_ctx *ctx, int64_t *launches);
+
+/* Message for an error code / the last error of a context (never NULL). */
+const char *pic_strerror(int code);
+const char *pic_last_error(pic_ctx *ctx);
+
+/* Frees host state, CUDA graphs/events and the NCCL communicator.  The
+ * workspace stays owned by the caller.  NULL is accepted. */
+void pic_destroy(pic_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIC_H */

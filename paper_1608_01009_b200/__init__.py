@@ -1,0 +1,9 @@
+"""B200-native fp64 particle-in-cell step (arXiv 1608.01009 hot path).
+
+The product is libpic.so (CUDA, sm_100a) behind the C ABI in include/pic.h;
+this package is its thin ctypes binding.  No oracle import, no CPU fallback.
+"""
+from .pic import (  # noqa: F401
+    EXPORTS, FLAG_NAIVE, FLAG_NO_GRAPH, FLAG_PROFILE, PicConfig, PicError, Simulation, lib,
+    make_config, simulation_from_workload,
+)

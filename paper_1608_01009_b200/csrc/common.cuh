@@ -1,0 +1,60 @@
+// common.cuh -- device-side layout and helpers shared by the libpic kernels.
+//
+// HBM layout:
+//  * E/B: one allocation [6][Z][Y][X] fp64, order Ex,Ey,Ez,Bx,By,Bz, each
+//    component ghost-padded by G cells on every side (X = nx+2G rounded up
+//    to even, Y = ny+2G, Z = nz_local+2G), x fastest.  Ghost cells hold the
+//    periodic images of the interior, written by the producing kernel, so
+//    the particle kernels never wrap an index.
+//  * J: two such allocations [3][Z][Y][X] (ping-pong): the deposit of step
+//    n lands in J_cur (interior + ghosts); the E update folds the ghost
+//    images into the interior and zeroes J_next for step n+1.
+//  * particles: per species SoA fp64 x,y,z,ux,uy,uz + uint64 id, double
+//    buffered (A = state, B = sort target), cell-sorted every K steps.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pic {
+
+constexpr int kGhost = 2;   // G: CIC gather needs [-1, n], VB edges need [-1, n+1]
+
+// error bits of the sticky device error word
+enum : unsigned {
+    kErrDisplacement = 1u,
+    kErrNonFinite = 2u,
+    kErrCapacity = 4u,
+    kErrRange = 8u,
+};
+
+struct GridDev {
+    int nx, ny, nz;          // local interior cells (nz = slab thickness)
+    int X, Y, Z;             // padded extents
+    int64_t cs;              // component stride X*Y*Z
+    int k0;                  // global z index of the first local cell
+    int nz_global;
+    double dx, dy, dz;
+    double inv_dx, inv_dy, inv_dz;
+    double dt, c;
+    double Lx, Ly, Lz;       // global periodic lengths
+    int S;                   // supercell edge
+    int nsx, nsy, nsz;       // supercells per axis (local)
+    bool periodic_z_local;   // nranks == 1: z ghosts are local images
+};
+
+__host__ __device__ inline int64_t pidx(const GridDev &g, int i, int j, int k)
+{
+    return (int64_t)(i + kGhost) + (int64_t)g.X * ((int64_t)(j + kGhost) + (int64_t)g.Y * (int64_t)(k + kGhost));
+}
+
+struct ParticlesDev {
+    double *x, *y, *z, *ux, *uy, *uz;
+    uint64_t *id;
+};
+
+struct SpeciesDev {
+    double qw;        // q * w
+    double h;         // q dt / (2 m c)   (Boris half-kick coefficient)
+};
+
+}  // namespace pic

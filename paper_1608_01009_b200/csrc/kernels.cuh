@@ -1,0 +1,41 @@
+// kernels.cuh -- host-side launchers of the libpic kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace pic {
+
+// ---- fields.cu : Yee FDTD and ghost maintenance ----
+// B -= (c dt/2) curl E on the interior, result also stored to its ghost images.
+void launch_b_half(const GridDev &g, double *EB, cudaStream_t st);
+// E += c dt curl B - 4 pi dt J where J = sum of the ghost images of Jcur
+// (the fold); writes the folded J back into Jcur's interior,
+// stores E to its ghost images and zeroes every image of Jnext.
+void launch_e_full(const GridDev &g, double *EB, double *Jcur, double *Jnext, cudaStream_t st);
+// Copies interior values of `ncomp` components to their ghost images.
+void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st);
+
+// ---- push_naive.cu ----
+void launch_push_naive(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
+                       const ParticlesDev &out, int64_t n, const SpeciesDev &sp, bool copy_id,
+                       unsigned *err, cudaStream_t st);
+
+// ---- sort.cu : stable counting sort by (supercell, local cell) ----
+struct SortScratch {
+    uint32_t *key;       // [cap]
+    uint32_t *slot;      // [cap]
+    uint32_t *perm_tmp;  // [cap]
+    uint32_t *perm;      // [cap]
+    uint32_t *count;     // [ncells + 1]
+    uint32_t *start;     // [ncells + 1]
+    uint32_t *block_sums;// [scan blocks]
+};
+size_t scan_block_count(int64_t nitems);
+// Sorts n particles src -> dst (x,y,z,ux,uy,uz,id) and writes the supercell
+// offsets sc_off[0..n_sc] (int64).
+void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst, int64_t n,
+                    const SortScratch &s, int64_t *sc_off, unsigned *err, cudaStream_t st,
+                    int *launches);
+
+}  // namespace pic

@@ -1,0 +1,196 @@
+// particle_math.cuh -- per-particle arithmetic of the PIC step (device code).
+//
+// Each function restates the scheme of SURVEY.md sec. 8a (rows a3-a5) and
+// DESIGN.md sec. 3; the arithmetic is re-derived for the GPU (reciprocal
+// square roots, local cell coordinates, a predicated <=4-segment split)
+// rather than copied from the CPU oracle, with which it shares no code.
+#pragma once
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace pic {
+
+// CIC weights along one axis for the integer-node and the half-node
+// sub-grids ("standard cloud-in-cell particle form factor";
+// SURVEY.md a3): g in cell units; node index i and fraction f with
+// W_0 = 1 - f, W_1 = f.
+struct AxisW {
+    int i0, ih;        // first node of the integer / half-staggered sub-grid
+    double f0, fh;     // fractions
+};
+
+__device__ __forceinline__ AxisW axis_weights(double g)
+{
+    AxisW a;
+    const double fl = floor(g);
+    a.i0 = (int)fl;
+    a.f0 = g - fl;
+    const double gh = g - 0.5;
+    const double flh = floor(gh);
+    a.ih = (int)flh;
+    a.fh = gh - flh;
+    return a;
+}
+
+// Trilinear interpolation of one component from a padded array:
+// base points at node (i,j,k); sx = 1, sy = row stride, sz = plane stride.
+__device__ __forceinline__ double trilinear(const double *__restrict__ f, int64_t base,
+                                            int64_t sy, int64_t sz, double fx, double fy,
+                                            double fz)
+{
+    const double c00 = fma(fx, f[base + 1] - f[base], f[base]);
+    const double c10 = fma(fx, f[base + sy + 1] - f[base + sy], f[base + sy]);
+    const double c01 = fma(fx, f[base + sz + 1] - f[base + sz], f[base + sz]);
+    const double c11 = fma(fx, f[base + sy + sz + 1] - f[base + sy + sz], f[base + sy + sz]);
+    const double c0 = fma(fy, c10 - c00, c00);
+    const double c1 = fma(fy, c11 - c01, c01);
+    return fma(fz, c1 - c0, c0);
+}
+
+// Relativistic Boris rotation on u = gamma*beta (reading R1):
+// u- = u + hE, t = hB/gamma(u-), u' = u- + u- x t, s = 2/(1+t^2),
+// u+ = u- + s u' x t, u = u+ + hE.
+__device__ __forceinline__ void boris(double h, double ex, double ey, double ez, double bx,
+                                      double by, double bz, double &ux, double &uy,
+                                      double &uz)
+{
+    const double umx = fma(h, ex, ux), umy = fma(h, ey, uy), umz = fma(h, ez, uz);
+    const double ig = rsqrt(1.0 + (umx * umx + umy * umy + umz * umz));
+    const double hg = h * ig;
+    const double tx = hg * bx, ty = hg * by, tz = hg * bz;
+    const double upx = umx + (umy * tz - umz * ty);
+    const double upy = umy + (umz * tx - umx * tz);
+    const double upz = umz + (umx * ty - umy * tx);
+    const double s = 2.0 / (1.0 + (tx * tx + ty * ty + tz * tz));
+    const double ppx = umx + s * (upy * tz - upz * ty);
+    const double ppy = umy + s * (upz * tx - upx * tz);
+    const double ppz = umz + s * (upx * ty - upy * tx);
+    ux = fma(h, ex, ppx);
+    uy = fma(h, ey, ppy);
+    uz = fma(h, ez, ppz);
+}
+
+// Periodic wrap, reading R7: x >= L -> x - L; x < 0 -> x + L, and a sum
+// that rounds to L becomes 0.
+__device__ __forceinline__ double wrap_coord(double x, double L)
+{
+    if (x >= L) return x - L;
+    if (x < 0.0) {
+        const double r = x + L;
+        return r == L ? 0.0 : r;
+    }
+    return x;
+}
+
+// Villasenor-Buneman deposit of one straight in-cell segment
+// (PAPER.md:48).  P1, P2 are local coordinates inside the
+// segment's cell (components in [0,1] up to rounding); add(comp, di, dj, dk,
+// value) receives the 12 edge contributions, comp 0/1/2 = Jx/Jy/Jz and
+// (di,dj,dk) the node offset of the edge inside the cell.
+template <class Add>
+__device__ __forceinline__ void vb_segment(double p1x, double p1y, double p1z, double p2x,
+                                          double p2y, double p2z, double kx, double ky,
+                                          double kz, Add &&add)
+{
+    const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
+    const double mx = 0.5 * (p1x + p2x), my = 0.5 * (p1y + p2y), mz = 0.5 * (p1z + p2z);
+    const double fx = kx * Dx, fy = ky * Dy, fz = kz * Dz;
+    const double cxx = Dy * Dz * (1.0 / 12.0);
+    const double cyy = Dx * Dz * (1.0 / 12.0);
+    const double czz = Dx * Dy * (1.0 / 12.0);
+    const double nx = 1.0 - mx, ny = 1.0 - my, nz = 1.0 - mz;
+    add(0, 0, 0, 0, fx * fma(ny, nz, cxx));
+    add(0, 0, 1, 0, fx * fma(my, nz, -cxx));
+    add(0, 0, 0, 1, fx * fma(ny, mz, -cxx));
+    add(0, 0, 1, 1, fx * fma(my, mz, cxx));
+    add(1, 0, 0, 0, fy * fma(nx, nz, cyy));
+    add(1, 1, 0, 0, fy * fma(mx, nz, -cyy));
+    add(1, 0, 0, 1, fy * fma(nx, mz, -cyy));
+    add(1, 1, 0, 1, fy * fma(mx, mz, cyy));
+    add(2, 0, 0, 0, fz * fma(nx, ny, czz));
+    add(2, 1, 0, 0, fz * fma(mx, ny, -czz));
+    add(2, 0, 1, 0, fz * fma(nx, my, -czz));
+    add(2, 1, 1, 0, fz * fma(mx, my, czz));
+}
+
+// Full VB deposit of the move a -> b, both in cell units relative to the
+// start cell (a in [0,1)^3, b = a + displacement).  The path is cut where it
+// crosses the start cell's faces (<= 1 crossing per axis because |b-a| < 1),
+// crossing fractions tau_d = (plane - a_d)/(b_d - a_d) are visited in
+// ascending order, and each piece is deposited in its cell, tracked
+// combinatorially (cell offset +-1 on the crossed axis).  add2(comp, di, dj,
+// dk, value) receives offsets relative to the START cell (in [-1, 2]).
+// Returns the number of segments deposited.
+template <class Add>
+__device__ __forceinline__ int vb_deposit(double ax, double ay, double az, double bx,
+                                          double by, double bz, double kx, double ky,
+                                          double kz, Add &&add2)
+{
+    // crossing planes in local coordinates: 0 when leaving downward, 1 upward
+    const bool cxq = (bx < 0.0) || (bx >= 1.0);
+    const bool cyq = (by < 0.0) || (by >= 1.0);
+    const bool czq = (bz < 0.0) || (bz >= 1.0);
+    if (!(cxq | cyq | czq)) {
+        vb_segment(ax, ay, az, bx, by, bz, kx, ky, kz,
+                   [&](int c, int di, int dj, int dk, double v) { add2(c, di, dj, dk, v); });
+        return 1;
+    }
+    const double px = bx < 0.0 ? 0.0 : 1.0, py = by < 0.0 ? 0.0 : 1.0, pz = bz < 0.0 ? 0.0 : 1.0;
+    double t[3];
+    int ax_id[3];
+    t[0] = cxq ? (px - ax) / (bx - ax) : 2.0; ax_id[0] = 0;
+    t[1] = cyq ? (py - ay) / (by - ay) : 2.0; ax_id[1] = 1;
+    t[2] = czq ? (pz - az) / (bz - az) : 2.0; ax_id[2] = 2;
+    // 3-element sorting network, ties keep axis order
+#define PIC_CSWAP(a_, b_)                                                   \
+    if (t[b_] < t[a_]) {                                                    \
+        double tt = t[a_]; t[a_] = t[b_]; t[b_] = tt;                       \
+        int ii = ax_id[a_]; ax_id[a_] = ax_id[b_]; ax_id[b_] = ii;          \
+    }
+    PIC_CSWAP(0, 1)
+    PIC_CSWAP(1, 2)
+    PIC_CSWAP(0, 1)
+#undef PIC_CSWAP
+    const double dx = bx - ax, dy = by - ay, dz = bz - az;
+    double sx = ax, sy = ay, sz = az;     // segment start, start-cell coordinates
+    int ox = 0, oy = 0, oz = 0;           // current cell offset
+    double tp = 0.0;
+    int nseg = 0;
+    for (int k = 0; k < 4; ++k) {
+        double ex, ey, ez, te;
+        int axis = -1;
+        if (k < 3 && t[k] <= 1.0) {
+            te = t[k];
+            axis = ax_id[k];
+            ex = fma(te, dx, ax);
+            ey = fma(te, dy, ay);
+            ez = fma(te, dz, az);
+            if (axis == 0) ex = px;
+            if (axis == 1) ey = py;
+            if (axis == 2) ez = pz;
+        } else {
+            te = 1.0;
+            ex = bx; ey = by; ez = bz;
+        }
+        if (te > tp) {
+            const double fox = (double)ox, foy = (double)oy, foz = (double)oz;
+            const int cox = ox, coy = oy, coz = oz;
+            vb_segment(sx - fox, sy - foy, sz - foz, ex - fox, ey - foy, ez - foz, kx, ky, kz,
+                       [&](int c, int di, int dj, int dk, double v) {
+                           add2(c, cox + di, coy + dj, coz + dk, v);
+                       });
+            ++nseg;
+        }
+        if (axis < 0) break;
+        if (axis == 0) ox += (dx > 0.0) ? 1 : -1;
+        if (axis == 1) oy += (dy > 0.0) ? 1 : -1;
+        if (axis == 2) oz += (dz > 0.0) ? 1 : -1;
+        sx = ex; sy = ey; sz = ez;
+        tp = te;
+    }
+    return nseg;
+}
+
+}  // namespace pic

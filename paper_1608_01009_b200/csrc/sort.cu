@@ -1,0 +1,232 @@
+// sort.cu -- stable counting sort of the particle store by
+// (supercell id, local cell id) (reading R15;
+// PAPER.md:40,44 "particles are stored separately for each cell",
+// PAPER.md:132 supercells).
+//
+// Deterministic and stable by construction:
+//   1. key[p] = key(x_p); slot[p] = atomicAdd(&count[key], 1)   (order within
+//      a bucket is arbitrary here)
+//   2. start = exclusive scan of count (3-kernel reduce / scan / add)
+//   3. perm_tmp[start[key] + slot] = p
+//   4. one warp per bucket re-orders its entries by ascending p (rank by
+//      counting) -> perm; this restores the input order inside each bucket,
+//      i.e. stability, independent of the atomic order in step 1
+//   5. gather x,y,z,ux,uy,uz,id through perm; sc_off[s] = start[s * S^3].
+// The key uses floor(x / dx) with an IEEE division, the same decision the
+// oracle takes (DESIGN.md sec. 3 R15), so permutations are bit-identical.
+#include "kernels.cuh"
+
+namespace pic {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+size_t scan_block_count(int64_t nitems) { return (size_t)((nitems + kScanTile - 1) / kScanTile); }
+
+__device__ __forceinline__ int cell_of(double x, double d, int n_local, int offset)
+{
+    int c = (int)floor(x / d) - offset;
+    c = c < 0 ? 0 : c;
+    return c >= n_local ? n_local - 1 : c;
+}
+
+__global__ void __launch_bounds__(256)
+k_sort_key(GridDev g, ParticlesDev src, int64_t n, uint32_t *__restrict__ key,
+           uint32_t *__restrict__ slot, uint32_t *__restrict__ count, unsigned *err)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double x = src.x[p], y = src.y[p], z = src.z[p];
+    if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= 0.0 && z < g.Lz))
+        atomicOr(err, isfinite(x) && isfinite(y) && isfinite(z) ? kErrRange : kErrNonFinite);
+    const int cx = cell_of(x, g.dx, g.nx, 0);
+    const int cy = cell_of(y, g.dy, g.ny, 0);
+    const int cz = cell_of(z, g.dz, g.nz, g.k0);
+    const int S = g.S;
+    const uint32_t sc = (uint32_t)((cx / S) + g.nsx * ((cy / S) + g.nsy * (cz / S)));
+    const uint32_t loc = (uint32_t)((cx % S) + S * ((cy % S) + S * (cz % S)));
+    const uint32_t k = sc * (uint32_t)(S * S * S) + loc;
+    key[p] = k;
+    slot[p] = atomicAdd(count + k, 1u);
+}
+
+// ---- exclusive scan of uint32 (counts fit: n < 2^31) ----
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// block-wide exclusive scan of one value per thread; returns block total in *total
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total)
+{
+    __shared__ uint32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t inc = warp_incl_scan(v);
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t s = lane < nw ? warp_sums[lane] : 0u;
+        s = warp_incl_scan(s);
+        warp_sums[lane] = s;
+    }
+    __syncthreads();
+    const uint32_t warp_prefix = wid ? warp_sums[wid - 1] : 0u;
+    *total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return warp_prefix + inc - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_reduce(const uint32_t *__restrict__ in, int64_t n, uint32_t *__restrict__ block_sums)
+{
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    uint32_t s = 0;
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        const int64_t i = base + (int64_t)it * kScanThreads + threadIdx.x;
+        if (i < n) s += in[i];
+    }
+    uint32_t total;
+    block_excl_scan(s, &total);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of the block sums in place
+__global__ void __launch_bounds__(kScanThreads) k_scan_blocks(uint32_t *__restrict__ sums, int64_t nb)
+{
+    uint32_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += kScanThreads) {
+        const int64_t i = b0 + threadIdx.x;
+        const uint32_t v = i < nb ? sums[i] : 0u;
+        uint32_t total;
+        const uint32_t ex = block_excl_scan(v, &total);
+        if (i < nb) sums[i] = carry + ex;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_add(const uint32_t *__restrict__ in, int64_t n, const uint32_t *__restrict__ block_off,
+           uint32_t *__restrict__ out)
+{
+    // each thread owns kScanItems consecutive elements
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        v[it] = (base + it < n) ? in[base + it] : 0u;
+        s += v[it];
+    }
+    uint32_t total;
+    uint32_t ex = block_excl_scan(s, &total) + block_off[blockIdx.x];
+#pragma unroll
+    for (int it = 0; it < kScanItems; ++it) {
+        if (base + it < n) out[base + it] = ex;
+        ex += v[it];
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_scatter(const uint32_t *__restrict__ key, const uint32_t *__restrict__ slot,
+          const uint32_t *__restrict__ start, int64_t n, uint32_t *__restrict__ perm_tmp)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    perm_tmp[start[key[p]] + slot[p]] = (uint32_t)p;
+}
+
+// one warp per bucket: perm[start + rank(v)] = v with rank = #{u < v}
+__global__ void __launch_bounds__(256)
+k_bucket_order(const uint32_t *__restrict__ start, int64_t nbuckets,
+               const uint32_t *__restrict__ perm_tmp, uint32_t *__restrict__ perm)
+{
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (b >= nbuckets) return;
+    const uint32_t s = start[b], e = start[b + 1];
+    const uint32_t m = e - s;
+    if (m == 0) return;
+    if (m == 1) {
+        if (lane == 0) perm[s] = perm_tmp[s];
+        return;
+    }
+    for (uint32_t i0 = 0; i0 < m; i0 += 32) {
+        const bool mine = i0 + lane < m;
+        const uint32_t v = mine ? perm_tmp[s + i0 + lane] : 0u;
+        uint32_t rank = 0;
+        for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+            const uint32_t u = (j0 + lane < m) ? perm_tmp[s + j0 + lane] : 0xffffffffu;
+            const uint32_t cnt = min(32u, m - j0);
+            for (uint32_t t = 0; t < cnt; ++t) {
+                const uint32_t ut = __shfl_sync(0xffffffffu, u, (int)t);
+                rank += (ut < v) ? 1u : 0u;
+            }
+        }
+        if (mine) perm[s + rank] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_gather(ParticlesDev src, ParticlesDev dst, const uint32_t *__restrict__ perm, int64_t n)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t p = perm[i];
+    dst.x[i] = src.x[p];
+    dst.y[i] = src.y[p];
+    dst.z[i] = src.z[p];
+    dst.ux[i] = src.ux[p];
+    dst.uy[i] = src.uy[p];
+    dst.uz[i] = src.uz[p];
+    dst.id[i] = src.id[p];
+}
+
+__global__ void k_sc_offsets(const uint32_t *__restrict__ start, int64_t n_sc, int cells_per_sc,
+                             int64_t *__restrict__ sc_off)
+{
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s > n_sc) return;
+    sc_off[s] = (int64_t)start[s * cells_per_sc];
+}
+
+void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst, int64_t n,
+                    const SortScratch &s, int64_t *sc_off, unsigned *err, cudaStream_t st,
+                    int *launches)
+{
+    const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
+    const int64_t n_sc = (int64_t)g.nsx * g.nsy * g.nsz;
+    const int64_t nscan = ncells + 1;   // count[ncells] stays 0 -> start[ncells] = n
+    int L = 0;
+    cudaMemsetAsync(s.count, 0, sizeof(uint32_t) * (size_t)nscan, st);
+    const int bs = 256;
+    if (n > 0) {
+        k_sort_key<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(g, src, n, s.key, s.slot, s.count, err);
+        ++L;
+    }
+    const int64_t nb = (int64_t)scan_block_count(nscan);
+    k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(s.count, nscan, s.block_sums);
+    k_scan_blocks<<<1, kScanThreads, 0, st>>>(s.block_sums, nb);
+    k_scan_add<<<(unsigned)nb, kScanThreads, 0, st>>>(s.count, nscan, s.block_sums, s.start);
+    L += 3;
+    if (n > 0) {
+        k_scatter<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(s.key, s.slot, s.start, n, s.perm_tmp);
+        const int64_t threads = ncells * 32;
+        k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);
+        k_gather<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(src, dst, s.perm, n);
+        L += 3;
+    }
+    k_sc_offsets<<<(unsigned)((n_sc + 1 + bs - 1) / bs), bs, 0, st>>>(s.start, n_sc, g.S * g.S * g.S, sc_off);
+    ++L;
+    if (launches) *launches += L;
+}
+
+}  // namespace pic

@@ -1,0 +1,236 @@
+"""Thin Python binding of libpic.so (include/pic.h).
+
+Argument marshalling only: every step of the PIC path runs in the CUDA
+kernels of libpic.so.  PyTorch provides the device workspace (one uint8 CUDA
+tensor), the CUDA stream and, for nranks > 1, the process group used to
+broadcast the NCCL id.  There is no CPU fallback: importing this module
+without libpic.so, or creating a Simulation without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpic.so")
+MAX_SPECIES = 4
+
+PIC_OK = 0
+ERRORS = {
+    -1: "PIC_EINVAL", -2: "PIC_ENOMEM", -3: "PIC_ECAPACITY", -4: "PIC_ESTATE",
+    -5: "PIC_EDISPLACEMENT", -6: "PIC_ENONFINITE", -7: "PIC_ECUDA", -8: "PIC_ENCCL",
+}
+FLAG_NO_GRAPH = 1
+FLAG_PROFILE = 2
+FLAG_NAIVE = 4
+
+EXPORTS = [
+    "pic_workspace_size", "pic_init", "pic_set_particles", "pic_set_fields", "pic_step",
+    "pic_get_fields", "pic_get_particles", "pic_get_count", "pic_get_step_index",
+    "pic_get_stage_times", "pic_get_launch_count", "pic_strerror", "pic_last_error",
+    "pic_destroy",
+]
+
+
+class PicConfig(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+        ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double),
+        ("dt", C.c_double), ("c", C.c_double),
+        ("n_species", C.c_int64),
+        ("q", C.c_double * MAX_SPECIES),
+        ("m", C.c_double * MAX_SPECIES),
+        ("w", C.c_double * MAX_SPECIES),
+        ("capacity", C.c_int64 * MAX_SPECIES),
+        ("supercell", C.c_int64),
+        ("sort_every", C.c_int64),
+        ("rank", C.c_int64), ("nranks", C.c_int64),
+        ("flags", C.c_int64),
+        ("nccl_id", C.c_uint8 * 128),
+        ("stream", C.c_void_p),
+    ]
+
+
+class PicError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libpic.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        dp, u64p, i64p = C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
+        cp = C.POINTER(PicConfig)
+        L.pic_workspace_size.argtypes = [cp, C.POINTER(C.c_size_t)]
+        L.pic_init.argtypes = [cp, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.pic_set_particles.argtypes = [C.c_void_p, C.c_int, C.c_int64, dp, dp, dp, dp, dp, dp, u64p]
+        L.pic_set_fields.argtypes = [C.c_void_p, dp]
+        L.pic_step.argtypes = [C.c_void_p, C.c_int64]
+        L.pic_get_fields.argtypes = [C.c_void_p, dp]
+        L.pic_get_particles.argtypes = [C.c_void_p, C.c_int, i64p, dp, dp, dp, dp, dp, dp, u64p]
+        L.pic_get_count.argtypes = [C.c_void_p, C.c_int, i64p]
+        L.pic_get_step_index.argtypes = [C.c_void_p, i64p]
+        L.pic_get_stage_times.argtypes = [C.c_void_p, dp, i64p]
+        L.pic_get_launch_count.argtypes = [C.c_void_p, i64p]
+        L.pic_strerror.argtypes = [C.c_int]
+        L.pic_strerror.restype = C.c_char_p
+        L.pic_last_error.argtypes = [C.c_void_p]
+        L.pic_last_error.restype = C.c_char_p
+        L.pic_destroy.argtypes = [C.c_void_p]
+        L.pic_destroy.restype = None
+        for name in EXPORTS:
+            if name not in ("pic_strerror", "pic_last_error", "pic_destroy"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _dptr(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity=None,
+                supercell=4, sort_every=20, rank=0, nranks=1, flags=0, nccl_id=None):
+    """species: list of (q, m, w)."""
+    cfg = PicConfig()
+    cfg.nx, cfg.ny, cfg.nz = nx, ny, nz
+    cfg.dx, cfg.dy, cfg.dz = dx, dy, dz
+    cfg.dt, cfg.c = dt, c
+    cfg.n_species = len(species)
+    for i, (q, m, w) in enumerate(species):
+        cfg.q[i], cfg.m[i], cfg.w[i] = q, m, w
+        cfg.capacity[i] = 0 if capacity is None else int(capacity[i])
+    cfg.supercell, cfg.sort_every = supercell, sort_every
+    cfg.rank, cfg.nranks, cfg.flags = rank, nranks, flags
+    if nccl_id is not None:
+        C.memmove(cfg.nccl_id, bytes(nccl_id), 128)
+    return cfg
+
+
+class Simulation:
+    """One libpic context on the current CUDA device.
+
+    Arrays cross the ABI as host numpy arrays (float64 / uint64); device
+    memory is a torch uint8 workspace; work runs on a dedicated torch stream."""
+
+    def __init__(self, cfg: PicConfig, device=None, stream=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("libpic needs a CUDA device (no CPU fallback)")
+        L = lib()
+        self.torch = torch
+        self.device = torch.device(device or "cuda")
+        self.stream = stream or torch.cuda.Stream(device=self.device)
+        cfg.stream = C.c_void_p(self.stream.cuda_stream)
+        self.cfg = cfg
+        nbytes = C.c_size_t(0)
+        self._check(L.pic_workspace_size(C.byref(cfg), C.byref(nbytes)), None)
+        self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) // 256 * 256
+        self.ctx = C.c_void_p()
+        with torch.cuda.device(self.device):
+            self._check(L.pic_init(C.byref(cfg), C.c_void_p(aligned), nbytes.value, C.byref(self.ctx)),
+                        None)
+        self.nx, self.ny, self.nz_local = cfg.nx, cfg.ny, cfg.nz // cfg.nranks
+
+    def _check(self, rc, ctx="self"):
+        if rc != PIC_OK:
+            L = lib()
+            msg = L.pic_strerror(rc).decode()
+            if ctx is not None and getattr(self, "ctx", None):
+                msg = L.pic_last_error(self.ctx).decode()
+            raise PicError(rc, msg)
+
+    def set_particles(self, species, P, ids):
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        n = P.shape[1]
+        rows = [np.ascontiguousarray(P[i]) for i in range(6)]
+        self._check(lib().pic_set_particles(self.ctx, species, n, *[_dptr(r) for r in rows],
+                                            ids.ctypes.data_as(C.POINTER(C.c_uint64))))
+
+    def set_fields(self, f6):
+        f6 = np.ascontiguousarray(f6, dtype=np.float64)
+        assert f6.size == 6 * self.nx * self.ny * self.nz_local
+        self._check(lib().pic_set_fields(self.ctx, _dptr(f6)))
+
+    def step(self, n=1):
+        self._check(lib().pic_step(self.ctx, int(n)))
+
+    def get_fields(self):
+        out = np.empty((9, self.nz_local, self.ny, self.nx), dtype=np.float64)
+        self._check(lib().pic_get_fields(self.ctx, _dptr(out)))
+        return out
+
+    def count(self, species):
+        n = C.c_int64(0)
+        self._check(lib().pic_get_count(self.ctx, species, C.byref(n)))
+        return n.value
+
+    def get_particles(self, species, out=None):
+        n = self.count(species)
+        if out is None:
+            P = np.empty((6, n), dtype=np.float64)
+            ids = np.empty(n, dtype=np.uint64)
+        else:
+            P, ids = out
+        cap = C.c_int64(P.shape[1])
+        self._check(lib().pic_get_particles(self.ctx, species, C.byref(cap),
+                                            *[_dptr(P[i]) for i in range(6)],
+                                            ids.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return P[:, :cap.value], ids[:cap.value]
+
+    def step_index(self):
+        n = C.c_int64(0)
+        self._check(lib().pic_get_step_index(self.ctx, C.byref(n)))
+        return n.value
+
+    def stage_times(self):
+        ms = (C.c_double * 4)()
+        nl = C.c_int64(0)
+        self._check(lib().pic_get_stage_times(self.ctx, ms, C.byref(nl)))
+        return {"sort": ms[0], "particle": ms[1], "field": ms[2], "exchange": ms[3],
+                "particle_launches": nl.value}
+
+    def launch_count(self):
+        n = C.c_int64(0)
+        self._check(lib().pic_get_launch_count(self.ctx, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().pic_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def simulation_from_workload(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
+                             sort_every=None, nccl_id=None, counts=None):
+    """Build a Simulation for a synth.Workload (species q, m, w, dt from the workload)."""
+    species = [(s.q, s.m, s.w) for s in wl.species]
+    nz_local = wl.nz // nranks
+    if counts is None:
+        counts = [s.ppc * wl.nx * wl.ny * nz_local for s in wl.species]
+    cap = [max(1, int(np.ceil(c * capacity_factor))) for c in counts]
+    cfg = make_config(wl.nx, wl.ny, wl.nz, species, wl.dt, wl.dx, wl.dy, wl.dz, wl.c, cap,
+                      supercell or wl.supercell,
+                      wl.sort_every if sort_every is None else sort_every,
+                      rank, nranks, flags, nccl_id)
+    return Simulation(cfg)

@@ -1,0 +1,311 @@
+"""GPU (libpic.so, through the C ABI) vs the CPU oracle on identical seeded
+inputs.  Tolerances from north_star (BASELINE.json:5) with reading R17:
+bit-exact sort permutation; <= 1e-12 per step (teacher-forced); <= 1e-9 after
+100 free-running steps."""
+import math
+
+import numpy as np
+import pytest
+
+from tests.helpers import by_id, compare_state, field_errs, pos_err, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-12
+TOL_FREE = 1e-9
+
+
+@pytest.fixture(scope="module")
+def pic():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1608_01009_b200 as P
+    P.lib()
+    return P
+
+
+def _oracle_for(O, wl, parts, sort_every=None, supercell=None):
+    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+               [O.Species(s.q, s.m, s.w) for s in wl.species],
+               supercell or wl.supercell, wl.sort_every if sort_every is None else sort_every)
+    return O.Oracle(g, particles=[(p.copy(), i.copy()) for p, i in parts])
+
+
+def _sim(pic, wl, flags=0, sort_every=None, supercell=None, capacity_factor=1.0, counts=None):
+    return pic.simulation_from_workload(wl, capacity_factor=capacity_factor, flags=flags,
+                                        sort_every=sort_every, supercell=supercell, counts=counts)
+
+
+def _load(sim, parts):
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+
+
+def _L(wl):
+    return (wl.nx * wl.dx, wl.ny * wl.dy, wl.nz * wl.dz)
+
+
+# ---------------------------------------------------------------- sort (a1)
+
+@pytest.mark.parametrize("S", [1, 2, 4])
+def test_sort_permutation_bit_exact(pic, oracle_mod, S):
+    from synth import get_config, gen_particles
+    wl = get_config("T_small").with_(supercell=S)
+    parts = gen_particles(wl)
+    P, ids = parts[0]
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(P.shape[1])          # scramble the input order
+    P, ids = P[:, perm].copy(), ids[perm].copy()
+    P[:3, ::5] = np.floor(P[:3, ::5])           # particles exactly on cell faces
+    P[:, 1::9] = P[:, 0::9][:, :P[:, 1::9].shape[1]]   # exact duplicates (ties)
+    orc = _oracle_for(oracle_mod, wl, [(P, ids)])
+    orc.sort()
+    sim = _sim(pic, wl)
+    sim.set_particles(0, P, ids)
+    gP, gids = sim.get_particles(0)
+    assert np.array_equal(gids, orc.ids[0])
+    assert np.array_equal(gP, orc.P[0])
+
+
+def test_sort_large_buckets_and_empty_cells(pic, oracle_mod):
+    from synth import get_config
+    wl = get_config("T_small").with_(supercell=2)
+    rng = np.random.default_rng(6)
+    n = 3000
+    P = np.zeros((6, n))
+    # 70% of the particles in 3 cells (buckets > 32 and > 1024 entries), rest spread
+    hot = rng.random(n) < 0.7
+    P[0] = np.where(hot, 3 + rng.random(n) * 0.999, rng.random(n) * 8)
+    P[1] = np.where(hot, 5.5, rng.random(n) * 12)
+    P[2] = np.where(hot, 7 + (rng.random(n) < 0.5), rng.random(n) * 16)
+    P[3:] = rng.standard_normal((3, n))
+    ids = rng.permutation(n).astype(np.uint64)
+    orc = _oracle_for(oracle_mod, wl, [(P, ids)])
+    orc.sort()
+    sim = _sim(pic, wl, counts=[n])
+    sim.set_particles(0, P, ids)
+    gP, gids = sim.get_particles(0)
+    assert np.array_equal(gids, orc.ids[0])
+    assert np.array_equal(gP, orc.P[0])
+
+
+# ---------------------------------------------------------------- fields (a7)
+
+def test_fdtd_random_fields_vs_oracle(pic, oracle_mod):
+    from synth import get_config
+    wl = get_config("T_small").with_(dx=1.1, dy=0.9, dz=1.3)
+    rng = np.random.default_rng(7)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx))
+    orc = _oracle_for(oracle_mod, wl, [(np.zeros((6, 0)), np.zeros(0, np.uint64))])
+    orc.F[:6] = F6
+    sim = _sim(pic, wl, counts=[0])
+    sim.set_fields(F6)
+    for _ in range(5):
+        orc.b_half(); orc.e_full(); orc.b_half()
+        sim.step(1)
+    G = sim.get_fields()
+    errs = field_errs(G[:6], orc.F[:6])
+    assert max(errs) <= TOL_STEP, errs
+    assert not G[6:].any()
+
+
+def test_vacuum_plane_wave_on_gpu(pic):
+    # discrete Yee eigenmode along z, E along x (closed form)
+    from synth import get_config
+    wl = get_config("T_small")
+    nz, dt = wl.nz, wl.dt
+    k = 2 * math.pi / nz
+    w = 2 / dt * math.asin(dt * math.sin(k / 2))
+    z = np.arange(nz)
+    F6 = np.zeros((6, wl.nz, wl.ny, wl.nx))
+    F6[0] = np.cos(k * z)[:, None, None]
+    F6[4] = (math.cos(w * dt / 2) * np.cos(k * (z + 0.5)))[:, None, None]
+    sim = _sim(pic, wl, counts=[0])
+    sim.set_fields(F6)
+    n = 200
+    sim.step(n)
+    G = sim.get_fields()
+    t = n * dt
+    np.testing.assert_allclose(G[0], np.broadcast_to(np.cos(k * z - w * t)[:, None, None], G[0].shape),
+                               rtol=0, atol=1e-12)
+    np.testing.assert_allclose(
+        G[4], np.broadcast_to((math.cos(w * dt / 2) * np.cos(k * (z + 0.5) - w * t))[:, None, None],
+                              G[4].shape), rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- whole step
+
+def _run_parity(pic, oracle_mod, wl, nsteps, teacher_forced, flags=0, fields=None, tol=TOL_STEP):
+    from synth import gen_particles
+    parts = gen_particles(wl)
+    orc = _oracle_for(oracle_mod, wl, parts)
+    if fields is not None:
+        orc.F[:6] = fields
+    sim = _sim(pic, wl, flags=flags)
+    L = _L(wl)
+    worst = 0.0
+    for step in range(nsteps):
+        if teacher_forced or step == 0:
+            sim.set_fields(orc.F[:6].copy())
+            for s in range(len(wl.species)):
+                sim.set_particles(s, orc.P[s], orc.ids[s])
+        orc.step(1)
+        sim.step(1)
+        G = sim.get_fields()
+        ferr = field_errs(G, orc.F)
+        errs = list(ferr)
+        for s in range(len(wl.species)):
+            gP, gi = sim.get_particles(s)
+            pe, ue = compare_state(gP, gi, orc.P[s], orc.ids[s], L)
+            errs += [pe, ue]
+        worst = max(worst, max(errs))
+        assert max(errs) <= tol, (step, errs)
+    return worst
+
+
+def test_c1_teacher_forced_per_step(pic, oracle_mod):
+    from synth import get_config
+    wl = get_config("C1")
+    _run_parity(pic, oracle_mod, wl, wl.steps, teacher_forced=True)
+
+
+def test_c1_free_running_matches_oracle(pic, oracle_mod):
+    from synth import get_config
+    wl = get_config("C1")
+    _run_parity(pic, oracle_mod, wl, 100, teacher_forced=False, tol=TOL_FREE)
+
+
+@pytest.mark.parametrize("name", ["T_small", "T_two_species"])
+def test_small_configs_free_running(pic, oracle_mod, name):
+    from synth import get_config
+    wl = get_config(name)
+    rng = np.random.default_rng(9)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.02
+    _run_parity(pic, oracle_mod, wl, 12, teacher_forced=False, fields=F6, tol=TOL_STEP * 100)
+
+
+def test_nonunit_cells_and_strong_fields(pic, oracle_mod):
+    from synth import get_config
+    wl = get_config("T_two_species").with_(dx=0.8, dy=1.2, dz=1.05, supercell=4)
+    rng = np.random.default_rng(10)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.5
+    _run_parity(pic, oracle_mod, wl, 6, teacher_forced=True, fields=F6)
+
+
+def test_naive_flag_path(pic, oracle_mod):
+    from synth import get_config
+    wl = get_config("T_small")
+    _run_parity(pic, oracle_mod, wl, 4, teacher_forced=True, flags=pic.FLAG_NAIVE)
+
+
+def test_frozen_plasma_bitwise(pic):
+    from synth import get_config, gen_particles
+    wl = get_config("C1").with_(species=(get_config("C1").species[0].__class__(
+        "electron", -1.0, 1.0, 8, 0.0),), sort_every=5)
+    parts = gen_particles(wl)
+    sim = _sim(pic, wl)
+    _load(sim, parts)
+    P0, i0 = sim.get_particles(0)
+    sim.step(23)
+    P1, i1 = sim.get_particles(0)
+    assert np.array_equal(i0, i1)
+    assert np.array_equal(P0, P1)
+    assert not sim.get_fields().any()
+
+
+# ---------------------------------------------------------------- edge cases
+
+def test_empty_species_and_capacity_errors(pic):
+    from synth import get_config, gen_particles
+    wl = get_config("T_two_species")
+    parts = gen_particles(wl)
+    sim = _sim(pic, wl)
+    sim.set_particles(0, *parts[0])            # species 1 stays empty
+    sim.step(3)
+    assert sim.count(1) == 0
+    big = np.zeros((6, parts[0][0].shape[1] + 1))
+    with pytest.raises(pic.PicError) as e:
+        sim.set_particles(0, big, np.zeros(big.shape[1], np.uint64))
+    assert e.value.code == -3
+    bad = parts[0][0].copy()
+    bad[0, 0] = wl.nx * wl.dx     # x == L is outside [0, L)
+    with pytest.raises(pic.PicError) as e:
+        sim.set_particles(0, bad, parts[0][1])
+    assert e.value.code == -1
+
+
+def test_nonfinite_momentum_is_reported(pic):
+    from synth import get_config, gen_particles
+    wl = get_config("T_small")
+    P, ids = gen_particles(wl)[0]
+    P = P.copy()
+    P[3, 7] = np.nan
+    sim = _sim(pic, wl)
+    sim.set_particles(0, P, ids)
+    with pytest.raises(pic.PicError) as e:
+        sim.step(1)
+    assert e.value.code == -6
+
+
+def test_cfl_violation_rejected(pic):
+    with pytest.raises(pic.PicError):
+        pic.Simulation(pic.make_config(8, 8, 8, [(-1.0, 1.0, 1.0)], dt=0.6, capacity=[10]))
+
+
+def test_tiny_grid_supercell_one(pic, oracle_mod):
+    from synth import Workload
+    from synth.configs import electron
+    wl = Workload("tiny", 2, 3, 1, (electron(5, 0.2),), steps=5, sort_every=2, supercell=1)
+    rng = np.random.default_rng(12)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.1
+    _run_parity(pic, oracle_mod, wl, 5, teacher_forced=False, fields=F6, tol=1e-11)
+
+
+# ---------------------------------------------------------------- full size (C2), sampled
+
+def test_c2_full_size_sampled_and_properties(pic, oracle_mod):
+    """C2 at full size in the bench launch configuration: after 25 steps,
+    (a) sampled particles' next step equals the oracle's per-particle gather/
+    Boris/move on the GPU's own fields; (b) continuity and total current hold
+    for the GPU's own deposit."""
+    from synth import get_config, gen_particles
+    wl = get_config("C2")
+    parts = gen_particles(wl)
+    sim = _sim(pic, wl)
+    _load(sim, parts)
+    sim.step(25)
+    F = sim.get_fields()
+    P0, i0 = sim.get_particles(0)
+    sim.step(1)
+    F1 = sim.get_fields()
+    P1, i1 = sim.get_particles(0)
+    # sort happens at step 40, not 25: same order
+    assert np.array_equal(i0, i1)
+    orc = _oracle_for(oracle_mod, wl, [(np.zeros((6, 0)), np.zeros(0, np.uint64))])
+    orc.F[:] = F
+    O = oracle_mod
+    sp = wl.species[0]
+    rng = np.random.default_rng(13)
+    sample = rng.choice(P0.shape[1], 2000, replace=False)
+    L = np.array(_L(wl))
+    for p in sample:
+        EB = orc.gather(*P0[:3, p])
+        u = O.boris(sp.q, sp.m, wl.c, wl.dt, EB, P0[3:, p])
+        xn = O.move(wl.c, wl.dt, u, P0[:3, p])
+        xn = np.array([O.wrap(xn[d], L[d]) for d in range(3)])
+        assert rel_err(P1[3:, p], u) <= TOL_STEP
+        d = (P1[:3, p] - xn + L / 2) % L - L / 2
+        assert np.abs(d).max() <= TOL_STEP * L.max()
+    # continuity with the GPU's J^{n+1/2} and positions
+    rho0 = orc.rho_of(0, P0)
+    rho1 = orc.rho_of(0, P1)
+    orc.F[6:] = F1[6:]
+    divj = orc.div_edge(6)
+    res = (rho1 - rho0) / wl.dt + divj
+    assert np.abs(res).max() <= 1e-12 * np.abs(divj).max() + 1e-15
+    # total current = sum q w v
+    v = (((P1[:3] - P0[:3]) + L[:, None] / 2) % L[:, None] - L[:, None] / 2) / wl.dt
+    tot = sp.q * sp.w * v.sum(axis=1)
+    got = F1[6:].sum(axis=(1, 2, 3))
+    np.testing.assert_allclose(got, tot, rtol=1e-9, atol=1e-12 * np.abs(tot).max())
