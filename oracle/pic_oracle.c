@@ -253,32 +253,55 @@ int64_t oracle_sort_key(const oracle_config *cfg, double x, double y, double z)
     return sc * S * S * S + local;
 }
 
-/* a1 -- stable counting sort of x,y,z,ux,uy,uz,id by the R15 key
- * (SPEC.md:298-306 re-binning). */
+/* a1 -- re-binning sort of x,y,z,ux,uy,uz,id (
+ * SPEC.md:298-306; reading R15 of DESIGN.md sec. 3).  Each particle gets
+ *   cell key = oracle_sort_key(x) = (supercell id, local cell id), and
+ *   slot     = number of particles with the same cell key before it in the
+ *              current array order,
+ * and the store is ordered by the unique triple (supercell id, slot, local
+ * cell id): inside a supercell the slot-0 particles of all its cells come
+ * first (in local cell order), then the slot-1 particles, and so on.
+ * The triple is unique per particle, so the order is fully determined. */
+typedef struct {
+    int64_t sc, slot, local, p;
+} sort_rec;
+
+static int cmp_rec(const void *a, const void *b)
+{
+    const sort_rec *x = (const sort_rec *)a, *y = (const sort_rec *)b;
+    if (x->sc != y->sc) return x->sc < y->sc ? -1 : 1;
+    if (x->slot != y->slot) return x->slot < y->slot ? -1 : 1;
+    if (x->local != y->local) return x->local < y->local ? -1 : 1;
+    return 0;
+}
+
 void oracle_sort(const oracle_config *cfg, int64_t n, double *P, uint64_t *id)
 {
     if (n <= 0)
         return;
     const int64_t nkeys = cfg->nx * cfg->ny * cfg->nz;
-    int64_t *key = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
-    int64_t *start = (int64_t *)calloc((size_t)nkeys + 1, sizeof(int64_t));
+    const int64_t S3 = cfg->supercell * cfg->supercell * cfg->supercell;
+    int64_t *seen = (int64_t *)calloc((size_t)nkeys, sizeof(int64_t));
+    sort_rec *rec = (sort_rec *)malloc(sizeof(sort_rec) * (size_t)n);
     double *tmp = (double *)malloc(sizeof(double) * 6 * (size_t)n);
     uint64_t *tid = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n);
     for (int64_t p = 0; p < n; ++p) {
-        key[p] = oracle_sort_key(cfg, P[p], P[n + p], P[2 * n + p]);
-        start[key[p] + 1] += 1;
+        int64_t key = oracle_sort_key(cfg, P[p], P[n + p], P[2 * n + p]);
+        rec[p].sc = key / S3;
+        rec[p].local = key % S3;
+        rec[p].slot = seen[key]++;
+        rec[p].p = p;
     }
-    for (int64_t k = 0; k < nkeys; ++k)
-        start[k + 1] += start[k];
-    for (int64_t p = 0; p < n; ++p) {
-        int64_t dst = start[key[p]]++;
+    qsort(rec, (size_t)n, sizeof(sort_rec), cmp_rec);
+    for (int64_t dst = 0; dst < n; ++dst) {
+        int64_t src = rec[dst].p;
         for (int c = 0; c < 6; ++c)
-            tmp[c * n + dst] = P[c * n + p];
-        tid[dst] = id[p];
+            tmp[c * n + dst] = P[c * n + src];
+        tid[dst] = id[src];
     }
     memcpy(P, tmp, sizeof(double) * 6 * (size_t)n);
     memcpy(id, tid, sizeof(uint64_t) * (size_t)n);
-    free(key); free(start); free(tmp); free(tid);
+    free(seen); free(rec); free(tmp); free(tid);
 }
 
 /* a7 / O3 -- B -= (c dt / 2) curl E, curl E evaluated at the B locations

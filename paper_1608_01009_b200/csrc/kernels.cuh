@@ -21,6 +21,13 @@ void launch_push_naive(const GridDev &g, const double *EB, double *J, const Part
                        const ParticlesDev &out, int64_t n, const SpeciesDev &sp, bool copy_id,
                        unsigned *err, cudaStream_t st);
 
+// ---- push_tile.cu : fused supercell kernel ----
+bool tile_supported(int S);
+void configure_tile_kernels();
+void launch_push_tile(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
+                      const ParticlesDev &out, const int64_t *sc_off, const SpeciesDev &sp,
+                      bool copy_id, unsigned *err, cudaStream_t st);
+
 // ---- sort.cu : stable counting sort by (supercell, local cell) ----
 struct SortScratch {
     uint32_t *key;       // [cap]

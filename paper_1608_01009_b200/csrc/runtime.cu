@@ -162,6 +162,7 @@ struct pic_ctx {
     SortScratch sort{};
     unsigned *err = nullptr;
     int64_t step_index = 0;
+    bool use_tile = false;     // fused supercell kernel (else the naive kernel)
     std::string last_error;
     // graphs keyed by (sort_now, jcur)
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -245,8 +246,13 @@ int enqueue_step(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
             SpeciesDev sp;
             sp.qw = ctx->cfg.q[s] * ctx->cfg.w[s];
             sp.h = ctx->cfg.q[s] * g.dt / (2.0 * ctx->cfg.m[s] * g.c);
-            launch_push_naive(g, ctx->EB, ctx->J[jcur], sort_now ? ctx->B[s] : ctx->A[s], ctx->A[s],
-                              ctx->count[s], sp, sort_now, ctx->err, ctx->st);
+            const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
+            if (ctx->use_tile)
+                launch_push_tile(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s], sp,
+                                 sort_now, ctx->err, ctx->st);
+            else
+                launch_push_naive(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->count[s], sp,
+                                  sort_now, ctx->err, ctx->st);
             ++launches;
             if (profile) ctx->particle_launches++;
         }
@@ -342,6 +348,8 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->sort.start = (uint32_t *)(ctx->ws + L.off_start);
     ctx->sort.block_sums = (uint32_t *)(ctx->ws + L.off_bsums);
     ctx->err = (unsigned *)(ctx->ws + L.off_err);
+    ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell);
+    configure_tile_kernels();
     // zero fields, offsets and the error word (particle arrays stay garbage until set)
     cudaError_t e = cudaMemsetAsync(ctx->ws, 0, L.off_sp[0][0], ctx->st);
     for (int s = 0; e == cudaSuccess && s < cfg->n_species; ++s)

@@ -1,5 +1,5 @@
-// sort.cu -- stable counting sort of the particle store by
-// (supercell id, local cell id) (reading R15;
+// sort.cu -- re-binning sort of the particle store by
+// (supercell id, slot, local cell id) (reading R15;
 // PAPER.md:40,44 "particles are stored separately for each cell",
 // PAPER.md:132 supercells).
 //
@@ -11,7 +11,12 @@
 //   4. one warp per bucket re-orders its entries by ascending p (rank by
 //      counting) -> perm; this restores the input order inside each bucket,
 //      i.e. stability, independent of the atomic order in step 1
-//   5. gather x,y,z,ux,uy,uz,id through perm; sc_off[s] = start[s * S^3].
+//   5. per supercell (one CTA), cell-sorted position (c, r) -> slot-major
+//      position sum_c' min(n_c', r) + #{c' < c : n_c' > r}, so a warp of
+//      consecutive particles holds distinct cells (conflict-free shared
+//      atomics in the deposit)
+//   6. gather x,y,z,ux,uy,uz,id through the final permutation;
+//      sc_off[s] = start[s * S^3].
 // The key uses floor(x / dx) with an IEEE division, the same decision the
 // oracle takes (DESIGN.md sec. 3 R15), so permutations are bit-identical.
 #include "kernels.cuh"
@@ -175,6 +180,40 @@ k_bucket_order(const uint32_t *__restrict__ start, int64_t nbuckets,
     }
 }
 
+// one CTA per supercell: perm (cell-sorted, stable) -> out (slot-major)
+__global__ void __launch_bounds__(256)
+k_interleave(const uint32_t *__restrict__ start, int cps, const uint32_t *__restrict__ perm,
+             uint32_t *__restrict__ out)
+{
+    extern __shared__ uint32_t sh[];
+    uint32_t *cnt = sh;            // [cps]
+    uint32_t *cum = sh + cps;      // [cps + 1], cell-sorted offsets inside the supercell
+    const int64_t c0 = (int64_t)blockIdx.x * cps;
+    const uint32_t base = start[c0];
+    for (int c = threadIdx.x; c <= cps; c += blockDim.x) {
+        cum[c] = start[c0 + c] - base;
+        if (c < cps) cnt[c] = start[c0 + c + 1] - start[c0 + c];
+    }
+    __syncthreads();
+    const uint32_t n = cum[cps];
+    for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
+        // cell of q: last c with cum[c] <= q (binary search over cps+1 offsets)
+        int lo = 0, hi = cps;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cum[mid] <= q) lo = mid; else hi = mid;
+        }
+        const int c = lo;
+        const uint32_t r = q - cum[c];
+        uint32_t pos = 0;
+        for (int cc = 0; cc < cps; ++cc) {
+            const uint32_t m = cnt[cc];
+            pos += min(m, r) + ((cc < c && m > r) ? 1u : 0u);
+        }
+        out[base + pos] = perm[base + q];
+    }
+}
+
 __global__ void __launch_bounds__(256)
 k_gather(ParticlesDev src, ParticlesDev dst, const uint32_t *__restrict__ perm, int64_t n)
 {
@@ -221,8 +260,11 @@ void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDe
         k_scatter<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(s.key, s.slot, s.start, n, s.perm_tmp);
         const int64_t threads = ncells * 32;
         k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);
-        k_gather<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(src, dst, s.perm, n);
-        L += 3;
+        const int cps = g.S * g.S * g.S;
+        k_interleave<<<(unsigned)n_sc, bs, sizeof(uint32_t) * (2 * cps + 1), st>>>(s.start, cps, s.perm,
+                                                                               s.perm_tmp);
+        k_gather<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(src, dst, s.perm_tmp, n);
+        L += 4;
     }
     k_sc_offsets<<<(unsigned)((n_sc + 1 + bs - 1) / bs), bs, 0, st>>>(s.start, n_sc, g.S * g.S * g.S, sc_off);
     ++L;

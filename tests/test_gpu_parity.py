@@ -193,6 +193,15 @@ def test_nonunit_cells_and_strong_fields(pic, oracle_mod):
     _run_parity(pic, oracle_mod, wl, 6, teacher_forced=True, fields=F6)
 
 
+def test_tile_fallback_after_long_drift(pic, oracle_mod):
+    """No re-sort for 30 steps at sigma 0.3: particles drift beyond the
+    tile halo and take the global fallback path of the fused kernel."""
+    from synth import get_config
+    from synth.configs import electron
+    wl = get_config("C1").with_(species=(electron(4, 0.3),), sort_every=0, nx=16, ny=16, nz=8)
+    _run_parity(pic, oracle_mod, wl, 30, teacher_forced=False, tol=1e-10)
+
+
 def test_naive_flag_path(pic, oracle_mod):
     from synth import get_config
     wl = get_config("T_small")

@@ -428,9 +428,21 @@ def test_p13_sort_is_stable_key_sort(oracle_mod):
     loc = (c[0] % S) + S * ((c[1] % S) + S * (c[2] % S))
     assert np.array_equal(keys, sc * 64 + loc)
     orc.sort()
-    perm = np.argsort(keys, kind="stable")
+    # R15: order by (supercell, slot, local cell); slot = rank of the particle
+    # among earlier particles of the same cell (numpy stable argsort + cumcount)
+    cell_order = np.argsort(keys, kind="stable")
+    sk = keys[cell_order]
+    first = np.r_[0, np.flatnonzero(np.diff(sk)) + 1]
+    run_start = np.repeat(first, np.diff(np.r_[first, n]))
+    slot = np.empty(n, dtype=np.int64)
+    slot[cell_order] = np.arange(n) - run_start
+    perm = np.lexsort((keys % 64, slot, keys // 64))
     assert np.array_equal(orc.ids[0], ids[perm])
     assert np.array_equal(orc.P[0], P[:, perm])
+    # inside one (supercell, slot) group the cells are distinct and ascending
+    sk, ss = keys[perm], slot[perm]
+    grp = (sk[1:] // 64 == sk[:-1] // 64) & (ss[1:] == ss[:-1])
+    assert (sk[1:][grp] > sk[:-1][grp]).all()
 
 
 def test_sort_key_clamps_rounding(oracle_mod):
