@@ -55,6 +55,11 @@ struct ParticlesDev {
 struct SpeciesDev {
     double qw;        // q * w
     double h;         // q dt / (2 m c)   (Boris half-kick coefficient)
+    // max |u|^2 of the species (high 32 bits of the fp64 value, an upper
+    // bound): read from the previous step, produced for the next one.  Sets
+    // the fixed-point scale of the deposit tile (push_tile.cu).
+    const unsigned *u2max_in;
+    unsigned *u2max_out;
 };
 
 }  // namespace pic

@@ -1,5 +1,6 @@
 // kernels.cuh -- host-side launchers of the libpic kernels (internal).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -23,10 +24,13 @@ void launch_push_naive(const GridDev &g, const double *EB, double *J, const Part
 
 // ---- push_tile.cu : fused supercell kernel ----
 bool tile_supported(int S);
+int tile_extent(int S);   // E/B tile edge (nodes) = the TMA box edge
+// max |u|^2 of n particles -> *out (high 32 bits of the fp64 value)
+void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st);
 void configure_tile_kernels();
-void launch_push_tile(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
-                      const ParticlesDev &out, const int64_t *sc_off, const SpeciesDev &sp,
-                      bool copy_id, unsigned *err, cudaStream_t st);
+void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
+                      const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
+                      const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st);
 
 // ---- sort.cu : stable counting sort by (supercell, local cell) ----
 struct SortScratch {

@@ -115,82 +115,42 @@ __device__ __forceinline__ void vb_segment(double p1x, double p1y, double p1z, d
     add(2, 1, 1, 0, fz * fma(mx, my, czz));
 }
 
-// Full VB deposit of the move a -> b, both in cell units relative to the
-// start cell (a in [0,1)^3, b = a + displacement).  The path is cut where it
-// crosses the start cell's faces (<= 1 crossing per axis because |b-a| < 1),
-// crossing fractions tau_d = (plane - a_d)/(b_d - a_d) are visited in
-// ascending order, and each piece is deposited in its cell, tracked
-// combinatorially (cell offset +-1 on the crossed axis).  add2(comp, di, dj,
-// dk, value) receives offsets relative to the START cell (in [-1, 2]).
-// Returns the number of segments deposited.
-template <class Add>
-__device__ __forceinline__ int vb_deposit(double ax, double ay, double az, double bx,
-                                          double by, double bz, double kx, double ky,
-                                          double kz, Add &&add2)
+// First piece of the VB split of a -> b (start-cell coordinates, a in
+// [0,1)^3): the path up to the first face crossing (or all of it) ends at e.
+// Returns true when more of the path remains; then (r1, r2) is the remainder
+// in the coordinates of the next cell, which is offset (ox, oy, oz) from the
+// start cell.  Ties between axes resolve to the lowest axis, as in
+// vb_deposit.  A zero-length first piece (a on the crossed face) is e == a.
+__device__ __forceinline__ bool vb_first_piece(double ax, double ay, double az, double bx,
+                                               double by, double bz, double &ex, double &ey,
+                                               double &ez, double r1[3], double r2[3], int &ox,
+                                               int &oy, int &oz)
 {
-    // crossing planes in local coordinates: 0 when leaving downward, 1 upward
     const bool cxq = (bx < 0.0) || (bx >= 1.0);
     const bool cyq = (by < 0.0) || (by >= 1.0);
     const bool czq = (bz < 0.0) || (bz >= 1.0);
-    if (!(cxq | cyq | czq)) {
-        vb_segment(ax, ay, az, bx, by, bz, kx, ky, kz,
-                   [&](int c, int di, int dj, int dk, double v) { add2(c, di, dj, dk, v); });
-        return 1;
+    const bool crossing = cxq | cyq | czq;
+    ex = bx; ey = by; ez = bz;
+    ox = oy = oz = 0;
+    if (crossing) {
+        const double px = bx < 0.0 ? 0.0 : 1.0, py = by < 0.0 ? 0.0 : 1.0, pz = bz < 0.0 ? 0.0 : 1.0;
+        const double tx = cxq ? (px - ax) / (bx - ax) : 2.0;
+        const double ty = cyq ? (py - ay) / (by - ay) : 2.0;
+        const double tz = czq ? (pz - az) / (bz - az) : 2.0;
+        int axis = 0;
+        double t = tx;
+        if (ty < t) { t = ty; axis = 1; }
+        if (tz < t) { t = tz; axis = 2; }
+        ex = fma(t, bx - ax, ax);
+        ey = fma(t, by - ay, ay);
+        ez = fma(t, bz - az, az);
+        if (axis == 0) { ex = px; ox = (bx > ax) ? 1 : -1; }
+        if (axis == 1) { ey = py; oy = (by > ay) ? 1 : -1; }
+        if (axis == 2) { ez = pz; oz = (bz > az) ? 1 : -1; }
+        r1[0] = ex - (double)ox; r1[1] = ey - (double)oy; r1[2] = ez - (double)oz;
+        r2[0] = bx - (double)ox; r2[1] = by - (double)oy; r2[2] = bz - (double)oz;
     }
-    const double px = bx < 0.0 ? 0.0 : 1.0, py = by < 0.0 ? 0.0 : 1.0, pz = bz < 0.0 ? 0.0 : 1.0;
-    double t[3];
-    int ax_id[3];
-    t[0] = cxq ? (px - ax) / (bx - ax) : 2.0; ax_id[0] = 0;
-    t[1] = cyq ? (py - ay) / (by - ay) : 2.0; ax_id[1] = 1;
-    t[2] = czq ? (pz - az) / (bz - az) : 2.0; ax_id[2] = 2;
-    // 3-element sorting network, ties keep axis order
-#define PIC_CSWAP(a_, b_)                                                   \
-    if (t[b_] < t[a_]) {                                                    \
-        double tt = t[a_]; t[a_] = t[b_]; t[b_] = tt;                       \
-        int ii = ax_id[a_]; ax_id[a_] = ax_id[b_]; ax_id[b_] = ii;          \
-    }
-    PIC_CSWAP(0, 1)
-    PIC_CSWAP(1, 2)
-    PIC_CSWAP(0, 1)
-#undef PIC_CSWAP
-    const double dx = bx - ax, dy = by - ay, dz = bz - az;
-    double sx = ax, sy = ay, sz = az;     // segment start, start-cell coordinates
-    int ox = 0, oy = 0, oz = 0;           // current cell offset
-    double tp = 0.0;
-    int nseg = 0;
-    for (int k = 0; k < 4; ++k) {
-        double ex, ey, ez, te;
-        int axis = -1;
-        if (k < 3 && t[k] <= 1.0) {
-            te = t[k];
-            axis = ax_id[k];
-            ex = fma(te, dx, ax);
-            ey = fma(te, dy, ay);
-            ez = fma(te, dz, az);
-            if (axis == 0) ex = px;
-            if (axis == 1) ey = py;
-            if (axis == 2) ez = pz;
-        } else {
-            te = 1.0;
-            ex = bx; ey = by; ez = bz;
-        }
-        if (te > tp) {
-            const double fox = (double)ox, foy = (double)oy, foz = (double)oz;
-            const int cox = ox, coy = oy, coz = oz;
-            vb_segment(sx - fox, sy - foy, sz - foz, ex - fox, ey - foy, ez - foz, kx, ky, kz,
-                       [&](int c, int di, int dj, int dk, double v) {
-                           add2(c, cox + di, coy + dj, coz + dk, v);
-                       });
-            ++nseg;
-        }
-        if (axis < 0) break;
-        if (axis == 0) ox += (dx > 0.0) ? 1 : -1;
-        if (axis == 1) oy += (dy > 0.0) ? 1 : -1;
-        if (axis == 2) oz += (dz > 0.0) ? 1 : -1;
-        sx = ex; sy = ey; sz = ez;
-        tp = te;
-    }
-    return nseg;
+    return crossing;
 }
 
 }  // namespace pic

@@ -49,11 +49,23 @@ __device__ __forceinline__ void push_one_global(const GridDev &g, const double *
     const double kx = sp.qw / (g.dt * g.dy * g.dz);
     const double ky = sp.qw / (g.dt * g.dx * g.dz);
     const double kz = sp.qw / (g.dt * g.dx * g.dy);
-    const int64_t base = pidx(g, wx.i0, wy.i0, wz.i0);
-    vb_deposit(ax, ay, az, bxl, byl, bzl, kx, ky, kz,
-               [&](int c, int di, int dj, int dk, double v) {
-                   atomicAdd(J + c * cs + base + di + dj * sy + dk * sz, v);
-               });
+    // split at the start cell's faces piece by piece (<= 4 pieces), each
+    // deposited with fp64 global atomics in its cell
+    int64_t base = pidx(g, wx.i0, wy.i0, wz.i0);
+    double a0 = ax, a1 = ay, a2 = az, b0 = bxl, b1 = byl, b2 = bzl;
+#pragma unroll 1
+    for (int it = 0; it < 4; ++it) {
+        double e0, e1, e2, r1[3], r2[3];
+        int ox, oy, oz;
+        const bool more = vb_first_piece(a0, a1, a2, b0, b1, b2, e0, e1, e2, r1, r2, ox, oy, oz);
+        vb_segment(a0, a1, a2, e0, e1, e2, kx, ky, kz, [&](int c, int di, int dj, int dk, double v) {
+            atomicAdd(J + c * cs + base + di + dj * sy + dk * sz, v);
+        });
+        if (!more) break;
+        base += ox + oy * sy + oz * sz;
+        a0 = r1[0]; a1 = r1[1]; a2 = r1[2];
+        b0 = r2[0]; b1 = r2[1]; b2 = r2[2];
+    }
     x = wrap_coord(xn, g.Lx);
     y = wrap_coord(yn, g.Ly);
     z = wrap_coord(zn, g.Lz);

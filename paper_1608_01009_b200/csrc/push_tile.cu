@@ -1,25 +1,36 @@
 // push_tile.cu -- the fused supercell particle kernel (SURVEY.md sec. 8a rows
 // a2-a6; north_star subsystem (2)).
 //
-// One CTA per supercell of S^3 cells ("grouping and
-// processing particles by supercells ... chosen so that particle and grid
-// data processed during the particle push and current deposition stages fit"
-// on-chip).  The CTA
-//   1. stages the supercell's E/B tile plus a (1+H)-cell halo,
-//      (S+2H+2)^3 x 6 fp64, from the ghost-padded fields into shared memory,
-//      and zeroes a (S+2H+3)^3 x 3 fp64 J tile;
-//   2. streams its particles [sc_off[s], sc_off[s+1]) with coalesced loads
-//      (the sort stores them slot-major, so the lanes of a warp sit in
-//      distinct cells), gathers E/B from the tile, does Boris + move, and
-//      deposits Villasenor-Buneman currents into the J tile with shared-memory
-//      fp64 atomics (conflict-free across lanes in distinct cells);
-//   3. particles that drifted more than H cells out of their supercell since
+// Supercells of S^3 cells ("grouping and processing
+// particles by supercells ... chosen so that particle and grid data processed
+// during the particle push and current deposition stages fit" on-chip) are
+// processed by persistent CTAs (2 per SM), each walking a strided list of
+// supercells.  Per supercell the CTA
+//   1. has its E/B tile plus a (1+H)-cell halo, (S+2H+2)^3 x 6 fp64, loaded
+//      by ONE TMA tensor copy from the ghost-padded fields -- issued while the
+//      previous supercell is processed (double-buffered, mbarrier-tracked);
+//   2. streams its particles [sc_off[s], sc_off[s+1]) in chunks of 256 that
+//      TMA bulk copies (6 arrays) prefetch one chunk ahead into shared memory;
+//      the sort stores particles slot-major, so the lanes of a warp sit in
+//      distinct cells;
+//   3. gathers E/B from the tile, does Boris + move, stores x, u with
+//      coalesced stores, and deposits the Villasenor-Buneman currents into a
+//      deterministic fixed-point J tile with native u32 shared atomics;
+//      the rest of face-crossing paths is queued and deposited per supercell;
+//   4. particles that drifted more than H cells out of their supercell since
 //      the last sort take the global path (L2 gather + REDG deposit);
-//   4. flushes the non-zero J tile entries to the padded global J with REDG.
+//   5. flushes the non-zero J tile entries to the padded global J with REDG.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "push_global.cuh"
+#include "tma.cuh"
 
 namespace pic {
+
+constexpr int kTileThreads = 256;
+constexpr int kQueue = 160;            // per-supercell queue of path remainders (crossing particles)
+constexpr int kCtasPerSm = 2;
 
 template <int S, int H>
 struct TileGeom {
@@ -27,109 +38,372 @@ struct TileGeom {
     static constexpr int TJ = S + 2 * H + 3;   // J tile extent (nodes)
     static constexpr int NE = TE * TE * TE;
     static constexpr int NJ = TJ * TJ * TJ;
-    static constexpr size_t smem_bytes = sizeof(double) * (6 * NE + 3 * NJ);
+    // shared-memory layout (byte offsets, 128-B aligned where TMA writes)
+    static constexpr size_t off_eb = 0;                                        // [2][6][NE] fp64
+    static constexpr size_t off_part = off_eb + 2 * 6 * NE * sizeof(double);   // [2][6][threads] fp64
+    static constexpr size_t off_q = off_part + 2 * 6 * kTileThreads * sizeof(double);   // [6][kQueue] fp64
+    static constexpr size_t off_jt = off_q + 6 * kQueue * sizeof(double);      // [9][NJ] u32
+    static constexpr size_t off_qcell = off_jt + 9 * NJ * sizeof(unsigned);    // [kQueue] u32
+    static constexpr size_t off_misc = (off_qcell + (kQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
+    static constexpr size_t smem_bytes = off_misc + 2 * sizeof(uint64_t);      // 2 mbarriers
 };
 
-constexpr int kTileThreads = 256;
+// ---- deterministic fixed-point J tile ----------------------------------
+// A contribution w (fp64) is scaled by 2^F (power of two, chosen per launch
+// from the species' speed bound, see k_push_tile) and rounded to the integer
+// v with one fma against 1.5*2^52 (the low 52 mantissa bits then hold
+// 2^51 + v).  v is split into lo16 | mid16 | hi (signed) and added to three
+// u32 tile counters with native shared-memory integer atomics (ATOMS.ADD,
+// fire-and-forget) -- fp64 shared atomics are CAS loops on sm_100a.  The
+// counters cannot overflow for < 2^16 contributions per edge (a supercell
+// holding < 16384 particles); the sums are exact, so the tile is independent
+// of the order of the atomics.  The flush rebuilds the int64 sum and converts
+// back with the exact factor 2^-F.
+constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
+constexpr int64_t kMaxTileParticles = 16383;
+
+// rare path: a particle outside its tile (drifted > H cells since the sort)
+__device__ __forceinline__ void push_outside_tile(const GridDev &g, const double *EB, double *J,
+                                                  const SpeciesDev &sp, double &x, double &y,
+                                                  double &z, double &ux, double &uy, double &uz,
+                                                  unsigned *err)
+{
+    push_one_global(g, EB, J, sp, x, y, z, ux, uy, uz, err);
+}
+
+// Deposits one in-cell segment P1 -> P2 (local coordinates of the cell whose
+// J-tile index is jbase) with the 12 Villasenor-Buneman edge values of
+// SURVEY.md a5, each added to the fixed-point tile as computed (low register
+// pressure).  A segment whose values could exceed the fixed-point range (a
+// particle that sped up by more than the 2x headroom since the last step)
+// goes to the fp64 global J instead (REDG).
+template <int TJ, int NJ>
+__device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, int64_t gorigin,
+                                            const GridDev &g, double p1x, double p1y, double p1z,
+                                            double p2x, double p2y, double p2z, double kx,
+                                            double ky, double kz, double scale)
+{
+    constexpr int TJ2 = TJ * TJ;
+    const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
+    const double mx = 0.5 * (p1x + p2x), my = 0.5 * (p1y + p2y), mz = 0.5 * (p1z + p2z);
+    const double fx = kx * Dx, fy = ky * Dy, fz = kz * Dz;
+    const double cxx = Dy * Dz * (1.0 / 12.0);
+    const double cyy = Dx * Dz * (1.0 / 12.0);
+    const double czz = Dx * Dy * (1.0 / 12.0);
+    const double nx = 1.0 - mx, ny = 1.0 - my, nz = 1.0 - mz;
+    // |value| <= |f| (1 + 1/12): weights are products of numbers in [0,1], |c| <= 1/12
+    const double fmaxv = fmax(fabs(fx), fmax(fabs(fy), fabs(fz)));
+    if (!(fmaxv * (13.0 / 12.0) * scale < 140737488355328.0)) {   // 2^47
+        const int tx = jbase % TJ, ty = (jbase / TJ) % TJ, tz = jbase / TJ2;
+        const int64_t X = g.X, XY = (int64_t)g.X * g.Y, cs = g.cs;
+        double *b = J + gorigin + tx + X * ty + XY * tz;
+        atomicAdd(b, fx * fma(ny, nz, cxx));
+        atomicAdd(b + X, fx * fma(my, nz, -cxx));
+        atomicAdd(b + XY, fx * fma(ny, mz, -cxx));
+        atomicAdd(b + X + XY, fx * fma(my, mz, cxx));
+        atomicAdd(b + cs, fy * fma(nx, nz, cyy));
+        atomicAdd(b + cs + 1, fy * fma(mx, nz, -cyy));
+        atomicAdd(b + cs + XY, fy * fma(nx, mz, -cyy));
+        atomicAdd(b + cs + 1 + XY, fy * fma(mx, mz, cyy));
+        atomicAdd(b + 2 * cs, fz * fma(nx, ny, czz));
+        atomicAdd(b + 2 * cs + 1, fz * fma(mx, ny, -czz));
+        atomicAdd(b + 2 * cs + X, fz * fma(nx, my, -czz));
+        atomicAdd(b + 2 * cs + 1 + X, fz * fma(mx, my, czz));
+        return;
+    }
+    unsigned *b = jt + jbase;
+    auto add = [&](int off, double v) {
+        const long long bits = __double_as_longlong(fma(v, scale, kMagic));
+        const unsigned lo = (unsigned)bits;
+        const unsigned hi = ((unsigned)(bits >> 32) & 0xfffffu) - (1u << 19);
+        atomicAdd(b + off, lo & 0xffffu);
+        atomicAdd(b + 3 * NJ + off, lo >> 16);
+        atomicAdd(b + 6 * NJ + off, hi);
+    };
+    add(0, fx * fma(ny, nz, cxx));
+    add(TJ, fx * fma(my, nz, -cxx));
+    add(TJ2, fx * fma(ny, mz, -cxx));
+    add(TJ + TJ2, fx * fma(my, mz, cxx));
+    add(NJ, fy * fma(nx, nz, cyy));
+    add(NJ + 1, fy * fma(mx, nz, -cyy));
+    add(NJ + TJ2, fy * fma(nx, mz, -cyy));
+    add(NJ + 1 + TJ2, fy * fma(mx, mz, cyy));
+    add(2 * NJ, fz * fma(nx, ny, czz));
+    add(2 * NJ + 1, fz * fma(mx, ny, -czz));
+    add(2 * NJ + TJ, fz * fma(nx, my, -czz));
+    add(2 * NJ + 1 + TJ, fz * fma(mx, my, czz));
+}
+
+// Deposits the rest of a split path (<= 2 more face crossings) starting in
+// the cell with J-tile index jb; a, b in that cell's coordinates.
+template <int TJ, int NJ>
+__device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *J, int64_t gorigin,
+                                                  const GridDev &g, double a0, double a1,
+                                                  double a2, double b0, double b1, double b2,
+                                                  double kx, double ky, double kz, double scale)
+{
+#pragma unroll 1
+    for (int it = 0; it < 3; ++it) {
+        double e0, e1, e2, r1[3], r2[3];
+        int ox, oy, oz;
+        const bool more = vb_first_piece(a0, a1, a2, b0, b1, b2, e0, e1, e2, r1, r2, ox, oy, oz);
+        deposit_seg<TJ, NJ>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale);
+        if (!more) break;
+        jb += ox + TJ * (oy + TJ * oz);
+        a0 = r1[0]; a1 = r1[1]; a2 = r1[2];
+        b0 = r2[0]; b1 = r2[1]; b2 = r2[2];
+    }
+}
+
+// next non-empty supercell of this CTA's strided list after `sc` (or >= nsc)
+__device__ __forceinline__ int next_sc(int sc, int nsc, const int64_t *__restrict__ sc_off)
+{
+    sc += gridDim.x;
+    while (sc < nsc && sc_off[sc + 1] == sc_off[sc]) sc += gridDim.x;
+    return sc;
+}
 
 template <int S, int H>
-__global__ void __launch_bounds__(kTileThreads, 2)
-k_push_tile(GridDev g, const double *__restrict__ EB, double *__restrict__ J, ParticlesDev in,
-            ParticlesDev out, const int64_t *__restrict__ sc_off, SpeciesDev sp, int copy_id,
-            unsigned *err)
+__global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
+k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
+            double *__restrict__ J, ParticlesDev in, ParticlesDev out,
+            const int64_t *__restrict__ sc_off, SpeciesDev sp, int copy_id, unsigned *err)
 {
     using T = TileGeom<S, H>;
     constexpr int TE = T::TE, TJ = T::TJ, NE = T::NE, NJ = T::NJ;
-    extern __shared__ double smem[];
-    double *eb = smem;            // [6][TE][TE][TE]
-    double *jt = smem + 6 * NE;   // [3][TJ][TJ][TJ]
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *ebuf = (double *)(smem_raw + T::off_eb);       // [2][6][NE]
+    double *pbuf = (double *)(smem_raw + T::off_part);     // [2][6][threads], one slot per thread
+    double *q = (double *)(smem_raw + T::off_q);           // [6][kQueue]
+    unsigned *jt = (unsigned *)(smem_raw + T::off_jt);     // [3 chunks][3][TJ^3]
+    unsigned *qcell = (unsigned *)(smem_raw + T::off_qcell);
+    unsigned *qcount = qcell + kQueue;
+    uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);   // [2]
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nsc = g.nsx * g.nsy * g.nsz;
+    constexpr uint32_t kEbBytes = 6 * NE * sizeof(double);
 
-    const int sc = blockIdx.x;
-    const int scx = sc % g.nsx, scy = (sc / g.nsx) % g.nsy, scz = sc / (g.nsx * g.nsy);
-    // local-grid coordinates of the tile origin (same for the E/B and J tiles)
-    const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
-    const int64_t cs = g.cs;
+    // tile origin (local-grid cell coords of tile node (0,0,0)) of supercell sc
+    auto origin = [&](int sc_, int &ox, int &oy, int &oz) {
+        const int scx = sc_ % g.nsx, scy = (sc_ / g.nsx) % g.nsy, scz = sc_ / (g.nsx * g.nsy);
+        ox = scx * S - H - 1;
+        oy = scy * S - H - 1;
+        oz = scz * S - H - 1;
+    };
+    auto issue_eb = [&](int sc_, int buf) {   // thread 0 only
+        int ox, oy, oz;
+        origin(sc_, ox, oy, oz);
+        mbar_arrive_expect_tx(&bar_eb[buf], kEbBytes);
+        tma_load_4d(ebuf + buf * 6 * NE, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, &bar_eb[buf]);
+    };
+    // this thread's particle p -> its own staging slot of stage `st` (async, LDGSTS)
+    auto stage_particle = [&](int p, int st) {
+        double *d = pbuf + st * 6 * kTileThreads + tid;
+        cp_async8(d + 0 * kTileThreads, in.x + p);
+        cp_async8(d + 1 * kTileThreads, in.y + p);
+        cp_async8(d + 2 * kTileThreads, in.z + p);
+        cp_async8(d + 3 * kTileThreads, in.ux + p);
+        cp_async8(d + 4 * kTileThreads, in.uy + p);
+        cp_async8(d + 5 * kTileThreads, in.uz + p);
+    };
 
-    for (int t = threadIdx.x; t < 6 * NE; t += kTileThreads) {
-        const int comp = t / NE, r = t - comp * NE;
-        const int a = r % TE, b = (r / TE) % TE, c = r / (TE * TE);
-        eb[t] = EB[comp * cs + pidx(g, ox + a, oy + b, oz + c)];
+    int sc = blockIdx.x;
+    while (sc < nsc && sc_off[sc + 1] == sc_off[sc]) sc += gridDim.x;
+    if (tid == 0) {
+        mbar_init(&bar_eb[0], 1);
+        mbar_init(&bar_eb[1], 1);
+        fence_mbar_init();
+        if (sc < nsc) issue_eb(sc, 0);
     }
-    for (int t = threadIdx.x; t < 3 * NJ; t += kTileThreads) jt[t] = 0.0;
+    uint32_t kst = 0;   // staging stage of the particle processed next
+    if (sc < nsc && sc_off[sc] + tid < sc_off[sc + 1]) stage_particle((int)sc_off[sc] + tid, 0);
+    cp_async_commit();
+    for (int t = tid; t < 9 * NJ; t += kTileThreads) jt[t] = 0u;
+    if (tid == 0) *qcount = 0u;
     __syncthreads();
 
     const double kx = sp.qw / (g.dt * g.dy * g.dz);
     const double ky = sp.qw / (g.dt * g.dx * g.dz);
     const double kz = sp.qw / (g.dt * g.dx * g.dy);
     const double cdt = g.c * g.dt;
-    const int64_t p0 = sc_off[sc], p1 = sc_off[sc + 1];
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += kTileThreads) {
-        double x = in.x[p], y = in.y[p], z = in.z[p];
-        double ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
-        const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
-        const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
-        // tile-relative start cell; inside the tile when in [1, S + 2H] on every axis
-        const int tx = wx.i0 - ox, ty = wy.i0 - oy, tz = wz.i0 - oz;
-        const bool inside = (unsigned)(tx - 1) < (unsigned)(S + 2 * H) &&
-                            (unsigned)(ty - 1) < (unsigned)(S + 2 * H) &&
-                            (unsigned)(tz - 1) < (unsigned)(S + 2 * H);
-        if (inside) {
-            const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
-            constexpr int sy = TE, sz = TE * TE;
-            const double ex = trilinear(eb + 0 * NE, hx + sy * ty + sz * tz, sy, sz, wx.fh, wy.f0, wz.f0);
-            const double ey = trilinear(eb + 1 * NE, tx + sy * hy + sz * tz, sy, sz, wx.f0, wy.fh, wz.f0);
-            const double ez = trilinear(eb + 2 * NE, tx + sy * ty + sz * hz, sy, sz, wx.f0, wy.f0, wz.fh);
-            const double bx = trilinear(eb + 3 * NE, tx + sy * hy + sz * hz, sy, sz, wx.f0, wy.fh, wz.fh);
-            const double by = trilinear(eb + 4 * NE, hx + sy * ty + sz * hz, sy, sz, wx.fh, wy.f0, wz.fh);
-            const double bz = trilinear(eb + 5 * NE, hx + sy * hy + sz * tz, sy, sz, wx.fh, wy.fh, wz.f0);
-            boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
-            const double ig = rsqrt(1.0 + (ux * ux + uy * uy + uz * uz));
-            const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
-            const double bxl = xn * g.inv_dx - (double)wx.i0;
-            const double byl = yn * g.inv_dy - (double)wy.i0;
-            const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
-            if (fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0) {
-                const int jbase = tx + TJ * (ty + TJ * tz);
-                vb_deposit(wx.f0, wy.f0, wz.f0, bxl, byl, bzl, kx, ky, kz,
-                           [&](int c, int di, int dj, int dk, double v) {
-                               atomicAdd(jt + c * NJ + jbase + di + TJ * (dj + TJ * dk), v);
-                           });
-                x = wrap_coord(xn, g.Lx);
-                y = wrap_coord(yn, g.Ly);
-                z = wrap_coord(zn, g.Lz);
-            } else {
-                atomicOr(err, (isfinite(xn) && isfinite(yn) && isfinite(zn)) ? kErrDisplacement
-                                                                              : kErrNonFinite);
+    // fixed-point scale 2^F of this step: every contribution is bounded by
+    // |qw| c beta / (dx dy dz) * 13/12 with beta <= 2 x the largest beta of
+    // the previous step (from its max |u|^2); 2^F maps that bound to < 2^46
+    double scale, inv_scale;
+    {
+        const double u2 = __longlong_as_double(((unsigned long long)(*sp.u2max_in) << 32) | 0xffffffffull);
+        const double beta = fmax(1e-4, fmin(1.0, 2.0 * sqrt(u2 / (1.0 + u2))));
+        const double wmax = fabs(sp.qw) * g.c / (g.dx * g.dy * g.dz) * (13.0 / 12.0) * beta;
+        const int F = wmax > 0.0 ? min(1000, (int)floor(46.0 - log2(wmax))) : 1000;
+        scale = ldexp(1.0, F);
+        inv_scale = ldexp(1.0, -F);
+    }
+    double u2loc = 0.0;   // this thread's max |u|^2 after the push
+    const int64_t cs = g.cs;
+    const int64_t gsy = g.X, gsz = (int64_t)g.X * g.Y;
+
+    for (uint32_t i = 0; sc < nsc; ++i) {
+        const int sc_nx = next_sc(sc, nsc, sc_off);
+        if (tid == 0 && sc_nx < nsc) issue_eb(sc_nx, (i + 1) & 1);   // prefetch the next tile
+        mbar_wait(&bar_eb[i & 1], (i >> 1) & 1);
+        const double *eb = ebuf + (i & 1) * 6 * NE;
+        int ox, oy, oz;
+        origin(sc, ox, oy, oz);
+        const int64_t gorigin = pidx(g, ox, oy, oz);   // padded global index of tile node (0,0,0)
+        const int p0 = (int)sc_off[sc], p1 = (int)sc_off[sc + 1];
+        // more particles than the fixed-point counters can absorb: global path only
+        const bool tile_ok = (p1 - p0) <= kMaxTileParticles;
+        // a thread with no particle here still prefetches its first of the next supercell
+        if (p0 + tid >= p1) {
+            if (sc_nx < nsc && sc_off[sc_nx] + tid < sc_off[sc_nx + 1])
+                stage_particle((int)sc_off[sc_nx] + tid, kst);
+            cp_async_commit();
+        }
+
+        for (int p = p0 + tid; p < p1; p += kTileThreads) {
+            // prefetch this thread's next particle (this supercell's, else the next one's first)
+            const int pn = p + kTileThreads;
+            if (pn < p1)
+                stage_particle(pn, kst ^ 1);
+            else if (sc_nx < nsc && sc_off[sc_nx] + tid < sc_off[sc_nx + 1])
+                stage_particle((int)sc_off[sc_nx] + tid, kst ^ 1);
+            cp_async_commit();
+            cp_async_wait1();   // this particle's stage has landed
+            {
+                const double *pl = pbuf + kst * 6 * kTileThreads + tid;
+                kst ^= 1;
+                double x = pl[0], y = pl[kTileThreads], z = pl[2 * kTileThreads];
+                double ux = pl[3 * kTileThreads], uy = pl[4 * kTileThreads], uz = pl[5 * kTileThreads];
+                const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
+                const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
+                // tile-relative start cell; inside the tile when in [1, S + 2H] on every axis
+                const int tx = wx.i0 - ox, ty = wy.i0 - oy, tz = wz.i0 - oz;
+                const bool inside = (unsigned)(tx - 1) < (unsigned)(S + 2 * H) &&
+                                    (unsigned)(ty - 1) < (unsigned)(S + 2 * H) &&
+                                    (unsigned)(tz - 1) < (unsigned)(S + 2 * H);
+                if (inside && tile_ok) {
+                    const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
+                    constexpr int sy = TE, sz = TE * TE;
+                    const double ex = trilinear(eb + 0 * NE, hx + sy * ty + sz * tz, sy, sz, wx.fh, wy.f0, wz.f0);
+                    const double ey = trilinear(eb + 1 * NE, tx + sy * hy + sz * tz, sy, sz, wx.f0, wy.fh, wz.f0);
+                    const double ez = trilinear(eb + 2 * NE, tx + sy * ty + sz * hz, sy, sz, wx.f0, wy.f0, wz.fh);
+                    const double bx = trilinear(eb + 3 * NE, tx + sy * hy + sz * hz, sy, sz, wx.f0, wy.fh, wz.fh);
+                    const double by = trilinear(eb + 4 * NE, hx + sy * ty + sz * hz, sy, sz, wx.fh, wy.f0, wz.fh);
+                    const double bz = trilinear(eb + 5 * NE, hx + sy * hy + sz * tz, sy, sz, wx.fh, wy.fh, wz.f0);
+                    boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
+                    const double ig = rsqrt(1.0 + (ux * ux + uy * uy + uz * uz));
+                    const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
+                    // move endpoints in start-cell coordinates (a = fractional parts, exact)
+                    const double ax = wx.f0, ay = wy.f0, az = wz.f0;
+                    const double bxl = xn * g.inv_dx - (double)wx.i0;
+                    const double byl = yn * g.inv_dy - (double)wy.i0;
+                    const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
+                    out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
+                    u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+                    if (fabs(bxl - ax) < 1.0 && fabs(byl - ay) < 1.0 && fabs(bzl - az) < 1.0) {
+                        out.x[p] = wrap_coord(xn, g.Lx);
+                        out.y[p] = wrap_coord(yn, g.Ly);
+                        out.z[p] = wrap_coord(zn, g.Lz);
+                        const int jbase = tx + TJ * (ty + TJ * tz);
+                        double ex_, ey_, ez_, r1[3], r2[3];
+                        int cx, cy, cz;
+                        const bool more =
+                            vb_first_piece(ax, ay, az, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
+                        deposit_seg<TJ, NJ>(jt, jbase, J, gorigin, g, ax, ay, az, ex_, ey_, ez_, kx, ky, kz,
+                                            scale);
+                        if (more) {
+                            // the rest of a face-crossing path is deposited at the end of the
+                            // supercell, all queued paths together (keeps the loop convergent)
+                            const int jrem = jbase + cx + TJ * (cy + TJ * cz);
+                            const unsigned slot = atomicAdd(qcount, 1u);
+                            if (slot < (unsigned)kQueue) {
+                                q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
+                                q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
+                                qcell[slot] = (unsigned)jrem;
+                            } else {
+                                deposit_remainder<TJ, NJ>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0],
+                                                          r2[1], r2[2], kx, ky, kz, scale);
+                            }
+                        }
+                    } else {
+                        out.x[p] = x; out.y[p] = y; out.z[p] = z;
+                        atomicOr(err, (isfinite(xn) && isfinite(yn) && isfinite(zn)) ? kErrDisplacement
+                                                                                      : kErrNonFinite);
+                    }
+                } else {
+                    push_outside_tile(g, EB, J, sp, x, y, z, ux, uy, uz, err);
+                    out.x[p] = x; out.y[p] = y; out.z[p] = z;
+                    out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
+                    u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+                }
+                if (copy_id) out.id[p] = in.id[p];
             }
-        } else {
-            push_one_global(g, EB, J, sp, x, y, z, ux, uy, uz, err);
         }
-        out.x[p] = x; out.y[p] = y; out.z[p] = z;
-        out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
-        if (copy_id) out.id[p] = in.id[p];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < 3 * NJ; t += kTileThreads) {
-        const double v = jt[t];
-        if (v != 0.0) {
-            const int comp = t / NJ, r = t - comp * NJ;
-            const int a = r % TJ, b = (r / TJ) % TJ, c = r / (TJ * TJ);
-            atomicAdd(J + comp * cs + pidx(g, ox + a, oy + b, oz + c), v);
+        __syncthreads();   // all particles of the supercell pushed, the queue is complete
+        // queued path remainders of this supercell
+        const int nq = min(*qcount, (unsigned)kQueue);
+        for (int e = tid; e < nq; e += kTileThreads) {
+            const int jrem = (int)qcell[e];
+            deposit_remainder<TJ, NJ>(jt, jrem, J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
+                                      q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz,
+                                      scale);
         }
+        __syncthreads();
+        // flush the fixed-point tile to the fp64 global J and re-zero it
+        for (int t = tid; t < 3 * NJ; t += kTileThreads) {
+            const long long fx = (long long)(int)jt[6 * NJ + t] * 4294967296LL +
+                                 (long long)jt[3 * NJ + t] * 65536LL + (long long)jt[t];
+            if (fx != 0) {
+                const int comp = t / NJ, r = t - comp * NJ;
+                const int a = r % TJ, b = (r / TJ) % TJ, c = r / (TJ * TJ);
+                atomicAdd(J + comp * cs + gorigin + a + gsy * b + gsz * c, (double)fx * inv_scale);
+            }
+            jt[t] = 0u;   // chunk counters can be non-zero with a zero sum
+            jt[3 * NJ + t] = 0u;
+            jt[6 * NJ + t] = 0u;
+        }
+        if (tid == 0) *qcount = 0u;
+        __syncthreads();   // tile zeroed, E/B buffer (i & 1) free for the tile issued next iteration
+        sc = sc_nx;
     }
+    {
+        const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc) >> 32));
+        if (lane == 0 && hi) atomicMax(sp.u2max_out, hi);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_u2max(ParticlesDev P, int64_t n, unsigned *out)
+{
+    double m = 0.0;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, P.ux[p] * P.ux[p] + P.uy[p] * P.uy[p] + P.uz[p] * P.uz[p]);
+    const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(m) >> 32));
+    if ((threadIdx.x & 31) == 0 && hi) atomicMax(out, hi);
+}
+
+void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st)
+{
+    cudaMemsetAsync(out, 0, sizeof(unsigned), st);
+    if (n > 0) k_u2max<<<296, 256, 0, st>>>(P, n, out);
 }
 
 template <int S, int H>
-static void launch_tile(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
-                        const ParticlesDev &out, const int64_t *sc_off, const SpeciesDev &sp,
-                        bool copy_id, unsigned *err, cudaStream_t st)
+static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
+                        const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
+                        const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
-    const unsigned nsc = (unsigned)g.nsx * g.nsy * g.nsz;
-    k_push_tile<S, H><<<nsc, kTileThreads, smem, st>>>(g, EB, J, in, out, sc_off, sp, copy_id ? 1 : 0, err);
+    const int nsc = g.nsx * g.nsy * g.nsz;
+    // persistent (kCtasPerSm per SM walking strided supercell lists) unless
+    // num_sms <= 0, which launches one CTA per supercell
+    const int grid = num_sms > 0 ? std::min(nsc, kCtasPerSm * num_sms) : nsc;
+    k_push_tile<S, H><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
+                                                        copy_id ? 1 : 0, err);
 }
 
 bool tile_supported(int S) { return S == 2 || S == 4; }
+
+int tile_extent(int S) { return S + 2 * 1 + 2; }
 
 void configure_tile_kernels()
 {
@@ -139,14 +413,14 @@ void configure_tile_kernels()
                          (int)TileGeom<2, 1>::smem_bytes);
 }
 
-void launch_push_tile(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
-                      const ParticlesDev &out, const int64_t *sc_off, const SpeciesDev &sp,
-                      bool copy_id, unsigned *err, cudaStream_t st)
+void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
+                      const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
+                      const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st)
 {
     if (g.S == 4)
-        launch_tile<4, 1>(g, EB, J, in, out, sc_off, sp, copy_id, err, st);
+        launch_tile<4, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, num_sms, st);
     else if (g.S == 2)
-        launch_tile<2, 1>(g, EB, J, in, out, sc_off, sp, copy_id, err, st);
+        launch_tile<2, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, num_sms, st);
 }
 
 }  // namespace pic

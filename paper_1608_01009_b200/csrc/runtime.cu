@@ -8,9 +8,12 @@
 //       output A (in place), deposit into J_cur
 //   a7  B half, E full (+ J fold, zero J_next), B half (fields.cu)
 //   swap J_cur / J_next
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -34,7 +37,7 @@ struct Layout {
     int64_t cap_max = 0;
     size_t off_eb = 0, off_j[2] = {}, off_sp[PIC_MAX_SPECIES][2] = {}, off_scoff[PIC_MAX_SPECIES] = {};
     size_t off_key = 0, off_slot = 0, off_perm_tmp = 0, off_perm = 0, off_count = 0, off_start = 0,
-           off_bsums = 0, off_err = 0;
+           off_bsums = 0, off_err = 0, off_stat = 0;
     size_t total = 0;
 };
 
@@ -110,6 +113,7 @@ Layout make_layout(const pic_config *c)
     L.off_start = o; o = align_up(o + 4 * (size_t)(L.ncells + 1));
     L.off_bsums = o; o = align_up(o + 4 * scan_block_count(L.ncells + 1));
     L.off_err = o; o = align_up(o + 64);
+    L.off_stat = o; o = align_up(o + 2 * PIC_MAX_SPECIES * sizeof(unsigned));
     L.total = o;
     return L;
 }
@@ -161,8 +165,11 @@ struct pic_ctx {
     int64_t count[PIC_MAX_SPECIES] = {};
     SortScratch sort{};
     unsigned *err = nullptr;
+    unsigned *u2max[2] = {nullptr, nullptr};   // [parity][species], see SpeciesDev
     int64_t step_index = 0;
     bool use_tile = false;     // fused supercell kernel (else the naive kernel)
+    CUtensorMap eb_map;        // TMA descriptor of the padded E/B array [6][Z][Y][X]
+    int num_sms = 148;
     std::string last_error;
     // graphs keyed by (sort_now, jcur)
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -241,15 +248,19 @@ int enqueue_step(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
     }
     {
         StageMark m(ctx, 1, profile);
+        // u^2 bounds: this step reads parity jcur, writes parity 1 - jcur
+        cudaMemsetAsync(ctx->u2max[1 - jcur], 0, PIC_MAX_SPECIES * sizeof(unsigned), ctx->st);
         for (int s = 0; s < ctx->cfg.n_species; ++s) {
             if (ctx->count[s] == 0) continue;
             SpeciesDev sp;
             sp.qw = ctx->cfg.q[s] * ctx->cfg.w[s];
             sp.h = ctx->cfg.q[s] * g.dt / (2.0 * ctx->cfg.m[s] * g.c);
+            sp.u2max_in = ctx->u2max[jcur] + s;
+            sp.u2max_out = ctx->u2max[1 - jcur] + s;
             const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
             if (ctx->use_tile)
-                launch_push_tile(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s], sp,
-                                 sort_now, ctx->err, ctx->st);
+                launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s],
+                                 sp, sort_now, ctx->err, ctx->num_sms, ctx->st);
             else
                 launch_push_naive(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->count[s], sp,
                                   sort_now, ctx->err, ctx->st);
@@ -289,6 +300,31 @@ int build_graph(pic_ctx *ctx, bool sort_now, int jcur)
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
     ctx->graph_launches[sort_now][jcur] = n;
+    return PIC_OK;
+}
+
+// TMA tensor map of the E/B fields: 4-D (x, y, z, component), box = one
+// supercell tile with halo (tile_extent^3 x 6), no swizzle, no OOB fill
+// (the ghost layers make every box in bounds).
+int encode_eb_map(pic_ctx *ctx)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    const GridDev &g = ctx->L.g;
+    const cuuint32_t te = (cuuint32_t)tile_extent(g.S);
+    cuuint64_t dims[4] = {(cuuint64_t)g.X, (cuuint64_t)g.Y, (cuuint64_t)g.Z, 6};
+    cuuint64_t strides[3] = {sizeof(double) * (cuuint64_t)g.X, sizeof(double) * (cuuint64_t)g.X * g.Y,
+                             sizeof(double) * (cuuint64_t)g.cs};
+    cuuint32_t box[4] = {te, te, te, 6};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(&ctx->eb_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->EB, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled failed");
     return PIC_OK;
 }
 
@@ -348,13 +384,27 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->sort.start = (uint32_t *)(ctx->ws + L.off_start);
     ctx->sort.block_sums = (uint32_t *)(ctx->ws + L.off_bsums);
     ctx->err = (unsigned *)(ctx->ws + L.off_err);
+    ctx->u2max[0] = (unsigned *)(ctx->ws + L.off_stat);
+    ctx->u2max[1] = ctx->u2max[0] + PIC_MAX_SPECIES;
     ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell);
     configure_tile_kernels();
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
+        const char *pe = getenv("PIC_TILE_PERSISTENT");   // tuning knob: "0" = one CTA per supercell
+        if (pe && pe[0] == '0') ctx->num_sms = 0;
+    }
+    if (ctx->use_tile && encode_eb_map(ctx) != PIC_OK) {
+        delete ctx;
+        return PIC_ECUDA;
+    }
     // zero fields, offsets and the error word (particle arrays stay garbage until set)
     cudaError_t e = cudaMemsetAsync(ctx->ws, 0, L.off_sp[0][0], ctx->st);
     for (int s = 0; e == cudaSuccess && s < cfg->n_species; ++s)
         e = cudaMemsetAsync(ctx->sc_off[s], 0, sizeof(int64_t) * (size_t)(L.n_sc + 1), ctx->st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ctx->err, 0, 64, ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->u2max[0], 0, 2 * PIC_MAX_SPECIES * sizeof(unsigned), ctx->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
     if (e != cudaSuccess) {
         delete ctx;
@@ -390,6 +440,8 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
     int launches = 0;
     sort_particles(g, Bs, ctx->A[species], n, ctx->sort, ctx->sc_off[species], ctx->err, ctx->st,
                    &launches);
+    launch_u2max(ctx->A[species], n, ctx->u2max[ctx->jcur] + species, ctx->st);
+    ++launches;
     ctx->launches += launches;
     PIC_CUDA(ctx, cudaGetLastError());
     destroy_graphs(ctx);

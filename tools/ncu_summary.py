@@ -1,0 +1,48 @@
+#!/usr/bin/env python3
+"""Summarise an ncu report: key raw metrics, stall reasons, per-opcode samples."""
+import csv
+import subprocess
+import sys
+from collections import Counter
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, vals = rows[0], rows[2]
+d = dict(zip(hdr, vals))
+want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__thread_inst_executed_per_inst_executed.ratio",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+for w in want:
+    print(w.ljust(78), d.get(w))
+st = [(h, v) for h, v in zip(hdr, vals) if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")]
+st = sorted(st, key=lambda x: -float(x[1] or 0))
+print("stalls:", ", ".join(f"{h.replace('smsp__pcsamp_warps_issue_stalled_', '')}={v}" for h, v in st[:8]))
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+srows = list(csv.reader(src.splitlines()))
+h2 = srows[1]
+data = srows[2:]
+i_s = h2.index("Warp Stall Sampling (All Samples)")
+i_src = h2.index("Source")
+i_ex = h2.index("Instructions Executed")
+c, ex = Counter(), Counter()
+for r in data:
+    t = r[i_src].split()
+    if not t:
+        continue
+    op = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
+    op = op.split(".")[0]
+    c[op] += int(r[i_s] or 0)
+    ex[op] += int(r[i_ex] or 0)
+tot = sum(c.values()) or 1
+print("samples by opcode:", ", ".join(f"{op}={100 * v / tot:.1f}%({ex[op]})" for op, v in c.most_common(12)))
