@@ -24,7 +24,7 @@ void launch_push_naive(const GridDev &g, const double *EB, double *J, const Part
 
 // ---- push_tile.cu : fused supercell kernel ----
 bool tile_supported(int S);
-int tile_extent(int S);   // E/B tile edge (nodes) = the TMA box edge
+void tile_box(int S, int box[4]);   // TMA box of the E/B tile (x pitch, y, z, comps)
 // max |u|^2 of n particles -> *out (high 32 bits of the fp64 value)
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st);
 void configure_tile_kernels();

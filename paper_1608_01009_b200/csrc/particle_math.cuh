@@ -49,6 +49,33 @@ __device__ __forceinline__ double trilinear(const double *__restrict__ f, int64_
     return fma(fz, c1 - c0, c0);
 }
 
+// Branch-free 1/d and 1/sqrt(d) for d >= 1 (finite): hardware approximation
+// (MUFU.RCP64H / MUFU.RSQ64H, ~2^-22) refined by two Newton steps to full
+// fp64 accuracy (<= ~1 ulp).  Used where d = 1 + (non-negative) so no special
+// cases exist; keeps the push straight-line code (no slow-path calls) so two
+// particles' dependency chains interleave.
+__device__ __forceinline__ double rcp_ge1(double d)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+__device__ __forceinline__ double rsqrt_ge1(double d)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    const double hd = 0.5 * d;
+    r = r * fma(-hd * r, r, 1.5);
+    r = r * fma(-hd * r, r, 1.5);
+    // final correction step in residual form (y = r + r (1 - d r^2) / 2)
+    const double e = fma(-d * r, r, 1.0);
+    return fma(0.5 * r, e, r);
+}
+
 // Relativistic Boris rotation on u = gamma*beta (reading R1):
 // u- = u + hE, t = hB/gamma(u-), u' = u- + u- x t, s = 2/(1+t^2),
 // u+ = u- + s u' x t, u = u+ + hE.
@@ -57,13 +84,13 @@ __device__ __forceinline__ void boris(double h, double ex, double ey, double ez,
                                       double &uz)
 {
     const double umx = fma(h, ex, ux), umy = fma(h, ey, uy), umz = fma(h, ez, uz);
-    const double ig = rsqrt(1.0 + (umx * umx + umy * umy + umz * umz));
+    const double ig = rsqrt_ge1(1.0 + (umx * umx + umy * umy + umz * umz));
     const double hg = h * ig;
     const double tx = hg * bx, ty = hg * by, tz = hg * bz;
     const double upx = umx + (umy * tz - umz * ty);
     const double upy = umy + (umz * tx - umx * tz);
     const double upz = umz + (umx * ty - umy * tx);
-    const double s = 2.0 / (1.0 + (tx * tx + ty * ty + tz * tz));
+    const double s = 2.0 * rcp_ge1(1.0 + (tx * tx + ty * ty + tz * tz));
     const double ppx = umx + s * (upy * tz - upz * ty);
     const double ppy = umy + s * (upz * tx - upx * tz);
     const double ppz = umz + s * (upx * ty - upy * tx);
@@ -76,12 +103,9 @@ __device__ __forceinline__ void boris(double h, double ex, double ey, double ez,
 // that rounds to L becomes 0.
 __device__ __forceinline__ double wrap_coord(double x, double L)
 {
-    if (x >= L) return x - L;
-    if (x < 0.0) {
-        const double r = x + L;
-        return r == L ? 0.0 : r;
-    }
-    return x;
+    const double lo = x + L;   // selects, no branches
+    const double wl = (lo == L) ? 0.0 : lo;
+    return (x >= L) ? x - L : ((x < 0.0) ? wl : x);
 }
 
 // Villasenor-Buneman deposit of one straight in-cell segment

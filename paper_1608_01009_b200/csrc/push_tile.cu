@@ -1,22 +1,21 @@
 // push_tile.cu -- the fused supercell particle kernel (SURVEY.md sec. 8a rows
 // a2-a6; north_star subsystem (2)).
 //
-// Supercells of S^3 cells ("grouping and processing
-// particles by supercells ... chosen so that particle and grid data processed
-// during the particle push and current deposition stages fit" on-chip) are
-// processed by persistent CTAs (2 per SM), each walking a strided list of
-// supercells.  Per supercell the CTA
-//   1. has its E/B tile plus a (1+H)-cell halo, (S+2H+2)^3 x 6 fp64, loaded
-//      by ONE TMA tensor copy from the ghost-padded fields -- issued while the
-//      previous supercell is processed (double-buffered, mbarrier-tracked);
-//   2. streams its particles [sc_off[s], sc_off[s+1]) in chunks of 256 that
-//      TMA bulk copies (6 arrays) prefetch one chunk ahead into shared memory;
-//      the sort stores particles slot-major, so the lanes of a warp sit in
-//      distinct cells;
-//   3. gathers E/B from the tile, does Boris + move, stores x, u with
-//      coalesced stores, and deposits the Villasenor-Buneman currents into a
-//      deterministic fixed-point J tile with native u32 shared atomics;
-//      the rest of face-crossing paths is queued and deposited per supercell;
+// One CTA per supercell of S^3 cells ("grouping and
+// processing particles by supercells ... chosen so that particle and grid
+// data processed during the particle push and current deposition stages fit"
+// on-chip).  The CTA
+//   1. loads the supercell's E/B tile plus a (1+H)-cell halo,
+//      (S+2H+2)^3 x 6 fp64, with ONE TMA tensor copy (mbarrier-tracked) from
+//      the ghost-padded fields into a bank-conflict-padded shared tile;
+//   2. streams its particles [sc_off[s], sc_off[s+1]) through per-thread
+//      cp.async (LDGSTS) staging, one particle ahead; the sort stores them
+//      slot-major, so the lanes of a warp sit in distinct cells;
+//   3. gathers E/B from the tile, does Boris + move (straight-line code),
+//      stores x, u with coalesced stores, and deposits the Villasenor-Buneman
+//      currents into a deterministic fixed-point J tile with native u32
+//      shared atomics; the rest of face-crossing paths is queued and
+//      deposited after the particle loop;
 //   4. particles that drifted more than H cells out of their supercell since
 //      the last sort take the global path (L2 gather + REDG deposit);
 //   5. flushes the non-zero J tile entries to the padded global J with REDG.
@@ -29,23 +28,35 @@
 namespace pic {
 
 constexpr int kTileThreads = 256;
-constexpr int kQueue = 160;            // per-supercell queue of path remainders (crossing particles)
+constexpr int kQueue = 160;     // per-supercell queue of path remainders (crossing particles)
 constexpr int kCtasPerSm = 2;
 
+// Shared-memory tile geometry.  Row/plane pitches are padded so that the 32
+// lanes of a warp -- 32 consecutive cells of a 4x4x2 block of the supercell
+// under the slot-major particle order -- hit distinct banks: the E/B row pitch
+// is = 4 (mod 8) doubles (12 for S = 4) and the J (u32) pitches are 12 and
+// = 16 (mod 32).  The E/B pitch is the TMA box width (the extra nodes of the
+// box are out-of-bounds zero fill or unused).
 template <int S, int H>
 struct TileGeom {
     static constexpr int TE = S + 2 * H + 2;   // E/B tile extent (nodes)
     static constexpr int TJ = S + 2 * H + 3;   // J tile extent (nodes)
-    static constexpr int NE = TE * TE * TE;
-    static constexpr int NJ = TJ * TJ * TJ;
+    static constexpr int EPX = (S == 4) ? 12 : TE;            // E/B row pitch (doubles) = TMA box dim 0
+    static constexpr int EPY = EPX * TE;                       // E/B plane pitch
+    static constexpr int NE = EPY * TE;                        // E/B component stride
+    static constexpr int JPX = (S == 4) ? 12 : TJ;             // J row pitch (u32)
+    static constexpr int JPY = (S == 4) ? 112 : JPX * TJ;      // J plane pitch
+    static constexpr int NJ = JPY * TJ;                        // J component stride
+    static_assert(EPX >= TE && JPX >= TJ && JPY >= JPX * TJ, "pitches");
+    static_assert((EPX * 8) % 16 == 0, "TMA box row must be a multiple of 16 bytes");
     // shared-memory layout (byte offsets, 128-B aligned where TMA writes)
-    static constexpr size_t off_eb = 0;                                        // [2][6][NE] fp64
-    static constexpr size_t off_part = off_eb + 2 * 6 * NE * sizeof(double);   // [2][6][threads] fp64
-    static constexpr size_t off_q = off_part + 2 * 6 * kTileThreads * sizeof(double);   // [6][kQueue] fp64
+    static constexpr size_t off_eb = 0;                                        // [6][NE] fp64
+    static constexpr size_t off_part = off_eb + 6 * NE * sizeof(double);       // [2][6][threads] fp64
+    static constexpr size_t off_q = off_part + 12 * kTileThreads * sizeof(double);   // [6][kQueue] fp64
     static constexpr size_t off_jt = off_q + 6 * kQueue * sizeof(double);      // [9][NJ] u32
     static constexpr size_t off_qcell = off_jt + 9 * NJ * sizeof(unsigned);    // [kQueue] u32
     static constexpr size_t off_misc = (off_qcell + (kQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
-    static constexpr size_t smem_bytes = off_misc + 2 * sizeof(uint64_t);      // 2 mbarriers
+    static constexpr size_t smem_bytes = off_misc + sizeof(uint64_t);          // 1 mbarrier
 };
 
 // ---- deterministic fixed-point J tile ----------------------------------
@@ -73,17 +84,17 @@ __device__ __forceinline__ void push_outside_tile(const GridDev &g, const double
 
 // Deposits one in-cell segment P1 -> P2 (local coordinates of the cell whose
 // J-tile index is jbase) with the 12 Villasenor-Buneman edge values of
-// SURVEY.md a5, each added to the fixed-point tile as computed (low register
-// pressure).  A segment whose values could exceed the fixed-point range (a
-// particle that sped up by more than the 2x headroom since the last step)
-// goes to the fp64 global J instead (REDG).
-template <int TJ, int NJ>
+// SURVEY.md a5, each added to the fixed-point tile as computed.  A segment
+// whose values could exceed the fixed-point range (a particle that sped up by
+// more than the 2x headroom since the last step) goes to the fp64 global J
+// instead (REDG).
+template <class T>
 __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, int64_t gorigin,
                                             const GridDev &g, double p1x, double p1y, double p1z,
                                             double p2x, double p2y, double p2z, double kx,
                                             double ky, double kz, double scale)
 {
-    constexpr int TJ2 = TJ * TJ;
+    constexpr int PX = T::JPX, PY = T::JPY, NJ = T::NJ;
     const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
     const double mx = 0.5 * (p1x + p2x), my = 0.5 * (p1y + p2y), mz = 0.5 * (p1z + p2z);
     const double fx = kx * Dx, fy = ky * Dy, fz = kz * Dz;
@@ -94,7 +105,7 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
     // |value| <= |f| (1 + 1/12): weights are products of numbers in [0,1], |c| <= 1/12
     const double fmaxv = fmax(fabs(fx), fmax(fabs(fy), fabs(fz)));
     if (!(fmaxv * (13.0 / 12.0) * scale < 140737488355328.0)) {   // 2^47
-        const int tx = jbase % TJ, ty = (jbase / TJ) % TJ, tz = jbase / TJ2;
+        const int rem = jbase % PY, tx = rem % PX, ty = rem / PX, tz = jbase / PY;
         const int64_t X = g.X, XY = (int64_t)g.X * g.Y, cs = g.cs;
         double *b = J + gorigin + tx + X * ty + XY * tz;
         atomicAdd(b, fx * fma(ny, nz, cxx));
@@ -121,22 +132,22 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
         atomicAdd(b + 6 * NJ + off, hi);
     };
     add(0, fx * fma(ny, nz, cxx));
-    add(TJ, fx * fma(my, nz, -cxx));
-    add(TJ2, fx * fma(ny, mz, -cxx));
-    add(TJ + TJ2, fx * fma(my, mz, cxx));
+    add(PX, fx * fma(my, nz, -cxx));
+    add(PY, fx * fma(ny, mz, -cxx));
+    add(PX + PY, fx * fma(my, mz, cxx));
     add(NJ, fy * fma(nx, nz, cyy));
     add(NJ + 1, fy * fma(mx, nz, -cyy));
-    add(NJ + TJ2, fy * fma(nx, mz, -cyy));
-    add(NJ + 1 + TJ2, fy * fma(mx, mz, cyy));
+    add(NJ + PY, fy * fma(nx, mz, -cyy));
+    add(NJ + 1 + PY, fy * fma(mx, mz, cyy));
     add(2 * NJ, fz * fma(nx, ny, czz));
     add(2 * NJ + 1, fz * fma(mx, ny, -czz));
-    add(2 * NJ + TJ, fz * fma(nx, my, -czz));
-    add(2 * NJ + 1 + TJ, fz * fma(mx, my, czz));
+    add(2 * NJ + PX, fz * fma(nx, my, -czz));
+    add(2 * NJ + 1 + PX, fz * fma(mx, my, czz));
 }
 
 // Deposits the rest of a split path (<= 2 more face crossings) starting in
 // the cell with J-tile index jb; a, b in that cell's coordinates.
-template <int TJ, int NJ>
+template <class T>
 __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *J, int64_t gorigin,
                                                   const GridDev &g, double a0, double a1,
                                                   double a2, double b0, double b1, double b2,
@@ -147,20 +158,12 @@ __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *
         double e0, e1, e2, r1[3], r2[3];
         int ox, oy, oz;
         const bool more = vb_first_piece(a0, a1, a2, b0, b1, b2, e0, e1, e2, r1, r2, ox, oy, oz);
-        deposit_seg<TJ, NJ>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale);
+        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale);
         if (!more) break;
-        jb += ox + TJ * (oy + TJ * oz);
+        jb += ox + T::JPX * oy + T::JPY * oz;
         a0 = r1[0]; a1 = r1[1]; a2 = r1[2];
         b0 = r2[0]; b1 = r2[1]; b2 = r2[2];
     }
-}
-
-// next non-empty supercell of this CTA's strided list after `sc` (or >= nsc)
-__device__ __forceinline__ int next_sc(int sc, int nsc, const int64_t *__restrict__ sc_off)
-{
-    sc += gridDim.x;
-    while (sc < nsc && sc_off[sc + 1] == sc_off[sc]) sc += gridDim.x;
-    return sc;
 }
 
 template <int S, int H>
@@ -170,57 +173,45 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const int64_t *__restrict__ sc_off, SpeciesDev sp, int copy_id, unsigned *err)
 {
     using T = TileGeom<S, H>;
-    constexpr int TE = T::TE, TJ = T::TJ, NE = T::NE, NJ = T::NJ;
+    constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = kTileThreads;
+    constexpr int EPX = T::EPX, EPY = T::EPY, JPX = T::JPX, JPY = T::JPY;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *ebuf = (double *)(smem_raw + T::off_eb);       // [2][6][NE]
-    double *pbuf = (double *)(smem_raw + T::off_part);     // [2][6][threads], one slot per thread
+    double *eb = (double *)(smem_raw + T::off_eb);         // [6][TE][TE][EPX]
+    double *pbuf = (double *)(smem_raw + T::off_part);     // [2 stages][6][NT]
     double *q = (double *)(smem_raw + T::off_q);           // [6][kQueue]
-    unsigned *jt = (unsigned *)(smem_raw + T::off_jt);     // [3 chunks][3][TJ^3]
+    unsigned *jt = (unsigned *)(smem_raw + T::off_jt);     // [3 chunks][3][TJ][JPY/..]
     unsigned *qcell = (unsigned *)(smem_raw + T::off_qcell);
     unsigned *qcount = qcell + kQueue;
-    uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);   // [2]
+    uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);
     const int tid = threadIdx.x, lane = tid & 31;
-    const int nsc = g.nsx * g.nsy * g.nsz;
-    constexpr uint32_t kEbBytes = 6 * NE * sizeof(double);
+    const int sc = blockIdx.x;
+    const int p0 = (int)sc_off[sc], p1 = (int)sc_off[sc + 1];
+    if (p0 == p1) return;   // empty supercell (uniform per CTA)
 
-    // tile origin (local-grid cell coords of tile node (0,0,0)) of supercell sc
-    auto origin = [&](int sc_, int &ox, int &oy, int &oz) {
-        const int scx = sc_ % g.nsx, scy = (sc_ / g.nsx) % g.nsy, scz = sc_ / (g.nsx * g.nsy);
-        ox = scx * S - H - 1;
-        oy = scy * S - H - 1;
-        oz = scz * S - H - 1;
-    };
-    auto issue_eb = [&](int sc_, int buf) {   // thread 0 only
-        int ox, oy, oz;
-        origin(sc_, ox, oy, oz);
-        mbar_arrive_expect_tx(&bar_eb[buf], kEbBytes);
-        tma_load_4d(ebuf + buf * 6 * NE, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, &bar_eb[buf]);
-    };
-    // this thread's particle p -> its own staging slot of stage `st` (async, LDGSTS)
-    auto stage_particle = [&](int p, int st) {
-        double *d = pbuf + st * 6 * kTileThreads + tid;
-        cp_async8(d + 0 * kTileThreads, in.x + p);
-        cp_async8(d + 1 * kTileThreads, in.y + p);
-        cp_async8(d + 2 * kTileThreads, in.z + p);
-        cp_async8(d + 3 * kTileThreads, in.ux + p);
-        cp_async8(d + 4 * kTileThreads, in.uy + p);
-        cp_async8(d + 5 * kTileThreads, in.uz + p);
-    };
+    const int scx = sc % g.nsx, scy = (sc / g.nsx) % g.nsy, scz = sc / (g.nsx * g.nsy);
+    // local-grid coordinates of the tile origin (same for the E/B and J tiles)
+    const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
+    const int64_t gorigin = pidx(g, ox, oy, oz);   // padded global index of tile node (0,0,0)
 
-    int sc = blockIdx.x;
-    while (sc < nsc && sc_off[sc + 1] == sc_off[sc]) sc += gridDim.x;
     if (tid == 0) {
-        mbar_init(&bar_eb[0], 1);
-        mbar_init(&bar_eb[1], 1);
+        mbar_init(bar_eb, 1);
         fence_mbar_init();
-        if (sc < nsc) issue_eb(sc, 0);
+        mbar_arrive_expect_tx(bar_eb, 6 * NE * sizeof(double));
+        tma_load_4d(eb, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, bar_eb);
     }
-    uint32_t kst = 0;   // staging stage of the particle processed next
-    if (sc < nsc && sc_off[sc] + tid < sc_off[sc + 1]) stage_particle((int)sc_off[sc] + tid, 0);
+    auto stage = [&](int p, int st) {   // this thread's particle p -> its staging slot
+        double *d = pbuf + st * 6 * NT + tid;
+        cp_async8(d + 0 * NT, in.x + p);
+        cp_async8(d + 1 * NT, in.y + p);
+        cp_async8(d + 2 * NT, in.z + p);
+        cp_async8(d + 3 * NT, in.ux + p);
+        cp_async8(d + 4 * NT, in.uy + p);
+        cp_async8(d + 5 * NT, in.uz + p);
+    };
+    if (p0 + tid < p1) stage(p0 + tid, 0);
     cp_async_commit();
-    for (int t = tid; t < 9 * NJ; t += kTileThreads) jt[t] = 0u;
+    for (int t = tid; t < 9 * NJ; t += NT) jt[t] = 0u;
     if (tid == 0) *qcount = 0u;
-    __syncthreads();
 
     const double kx = sp.qw / (g.dt * g.dy * g.dz);
     const double ky = sp.qw / (g.dt * g.dx * g.dz);
@@ -239,132 +230,98 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         inv_scale = ldexp(1.0, -F);
     }
     double u2loc = 0.0;   // this thread's max |u|^2 after the push
-    const int64_t cs = g.cs;
-    const int64_t gsy = g.X, gsz = (int64_t)g.X * g.Y;
+    const bool tile_ok = (p1 - p0) <= kMaxTileParticles;   // else the counters could overflow
+    __syncthreads();
+    mbar_wait(bar_eb, 0);
 
-    for (uint32_t i = 0; sc < nsc; ++i) {
-        const int sc_nx = next_sc(sc, nsc, sc_off);
-        if (tid == 0 && sc_nx < nsc) issue_eb(sc_nx, (i + 1) & 1);   // prefetch the next tile
-        mbar_wait(&bar_eb[i & 1], (i >> 1) & 1);
-        const double *eb = ebuf + (i & 1) * 6 * NE;
-        int ox, oy, oz;
-        origin(sc, ox, oy, oz);
-        const int64_t gorigin = pidx(g, ox, oy, oz);   // padded global index of tile node (0,0,0)
-        const int p0 = (int)sc_off[sc], p1 = (int)sc_off[sc + 1];
-        // more particles than the fixed-point counters can absorb: global path only
-        const bool tile_ok = (p1 - p0) <= kMaxTileParticles;
-        // a thread with no particle here still prefetches its first of the next supercell
-        if (p0 + tid >= p1) {
-            if (sc_nx < nsc && sc_off[sc_nx] + tid < sc_off[sc_nx + 1])
-                stage_particle((int)sc_off[sc_nx] + tid, kst);
-            cp_async_commit();
-        }
-
-        for (int p = p0 + tid; p < p1; p += kTileThreads) {
-            // prefetch this thread's next particle (this supercell's, else the next one's first)
-            const int pn = p + kTileThreads;
-            if (pn < p1)
-                stage_particle(pn, kst ^ 1);
-            else if (sc_nx < nsc && sc_off[sc_nx] + tid < sc_off[sc_nx + 1])
-                stage_particle((int)sc_off[sc_nx] + tid, kst ^ 1);
-            cp_async_commit();
-            cp_async_wait1();   // this particle's stage has landed
-            {
-                const double *pl = pbuf + kst * 6 * kTileThreads + tid;
-                kst ^= 1;
-                double x = pl[0], y = pl[kTileThreads], z = pl[2 * kTileThreads];
-                double ux = pl[3 * kTileThreads], uy = pl[4 * kTileThreads], uz = pl[5 * kTileThreads];
-                const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
-                const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
-                // tile-relative start cell; inside the tile when in [1, S + 2H] on every axis
-                const int tx = wx.i0 - ox, ty = wy.i0 - oy, tz = wz.i0 - oz;
-                const bool inside = (unsigned)(tx - 1) < (unsigned)(S + 2 * H) &&
-                                    (unsigned)(ty - 1) < (unsigned)(S + 2 * H) &&
-                                    (unsigned)(tz - 1) < (unsigned)(S + 2 * H);
-                if (inside && tile_ok) {
-                    const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
-                    constexpr int sy = TE, sz = TE * TE;
-                    const double ex = trilinear(eb + 0 * NE, hx + sy * ty + sz * tz, sy, sz, wx.fh, wy.f0, wz.f0);
-                    const double ey = trilinear(eb + 1 * NE, tx + sy * hy + sz * tz, sy, sz, wx.f0, wy.fh, wz.f0);
-                    const double ez = trilinear(eb + 2 * NE, tx + sy * ty + sz * hz, sy, sz, wx.f0, wy.f0, wz.fh);
-                    const double bx = trilinear(eb + 3 * NE, tx + sy * hy + sz * hz, sy, sz, wx.f0, wy.fh, wz.fh);
-                    const double by = trilinear(eb + 4 * NE, hx + sy * ty + sz * hz, sy, sz, wx.fh, wy.f0, wz.fh);
-                    const double bz = trilinear(eb + 5 * NE, hx + sy * hy + sz * tz, sy, sz, wx.fh, wy.fh, wz.f0);
-                    boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
-                    const double ig = rsqrt(1.0 + (ux * ux + uy * uy + uz * uz));
-                    const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
-                    // move endpoints in start-cell coordinates (a = fractional parts, exact)
-                    const double ax = wx.f0, ay = wy.f0, az = wz.f0;
-                    const double bxl = xn * g.inv_dx - (double)wx.i0;
-                    const double byl = yn * g.inv_dy - (double)wy.i0;
-                    const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
-                    out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
-                    u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
-                    if (fabs(bxl - ax) < 1.0 && fabs(byl - ay) < 1.0 && fabs(bzl - az) < 1.0) {
-                        out.x[p] = wrap_coord(xn, g.Lx);
-                        out.y[p] = wrap_coord(yn, g.Ly);
-                        out.z[p] = wrap_coord(zn, g.Lz);
-                        const int jbase = tx + TJ * (ty + TJ * tz);
-                        double ex_, ey_, ez_, r1[3], r2[3];
-                        int cx, cy, cz;
-                        const bool more =
-                            vb_first_piece(ax, ay, az, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
-                        deposit_seg<TJ, NJ>(jt, jbase, J, gorigin, g, ax, ay, az, ex_, ey_, ez_, kx, ky, kz,
-                                            scale);
-                        if (more) {
-                            // the rest of a face-crossing path is deposited at the end of the
-                            // supercell, all queued paths together (keeps the loop convergent)
-                            const int jrem = jbase + cx + TJ * (cy + TJ * cz);
-                            const unsigned slot = atomicAdd(qcount, 1u);
-                            if (slot < (unsigned)kQueue) {
-                                q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
-                                q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
-                                qcell[slot] = (unsigned)jrem;
-                            } else {
-                                deposit_remainder<TJ, NJ>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0],
-                                                          r2[1], r2[2], kx, ky, kz, scale);
-                            }
-                        }
+    int st = 0;
+    for (int p = p0 + tid; p < p1; p += NT) {
+        if (p + NT < p1) stage(p + NT, st ^ 1);   // prefetch the next particle
+        cp_async_commit();
+        cp_async_wait1();
+        const double *pl = pbuf + st * 6 * NT + tid;
+        const double x = pl[0], y = pl[NT], z = pl[2 * NT];
+        double ux = pl[3 * NT], uy = pl[4 * NT], uz = pl[5 * NT];
+        const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
+        const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
+        // tile-relative start cell; inside the tile when in [1, S + 2H] on every axis
+        const int tx = wx.i0 - ox, ty = wy.i0 - oy, tz = wz.i0 - oz;
+        const bool inside = tile_ok && (unsigned)(tx - 1) < (unsigned)(S + 2 * H) &&
+                            (unsigned)(ty - 1) < (unsigned)(S + 2 * H) &&
+                            (unsigned)(tz - 1) < (unsigned)(S + 2 * H);
+        if (inside) {
+            const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
+            const double ex = trilinear(eb + 0 * NE, hx + EPX * ty + EPY * tz, EPX, EPY, wx.fh, wy.f0, wz.f0);
+            const double ey = trilinear(eb + 1 * NE, tx + EPX * hy + EPY * tz, EPX, EPY, wx.f0, wy.fh, wz.f0);
+            const double ez = trilinear(eb + 2 * NE, tx + EPX * ty + EPY * hz, EPX, EPY, wx.f0, wy.f0, wz.fh);
+            const double bx = trilinear(eb + 3 * NE, tx + EPX * hy + EPY * hz, EPX, EPY, wx.f0, wy.fh, wz.fh);
+            const double by = trilinear(eb + 4 * NE, hx + EPX * ty + EPY * hz, EPX, EPY, wx.fh, wy.f0, wz.fh);
+            const double bz = trilinear(eb + 5 * NE, hx + EPX * hy + EPY * tz, EPX, EPY, wx.fh, wy.fh, wz.f0);
+            boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
+            const double ig = rsqrt_ge1(1.0 + (ux * ux + uy * uy + uz * uz));
+            const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
+            // move endpoints in start-cell coordinates (a = fractional parts, exact)
+            const double bxl = xn * g.inv_dx - (double)wx.i0;
+            const double byl = yn * g.inv_dy - (double)wy.i0;
+            const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
+            const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
+            out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
+            out.x[p] = ok ? wrap_coord(xn, g.Lx) : x;
+            out.y[p] = ok ? wrap_coord(yn, g.Ly) : y;
+            out.z[p] = ok ? wrap_coord(zn, g.Lz) : z;
+            u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+            if (ok) {
+                const int jbase = tx + JPX * ty + JPY * tz;
+                double ex_, ey_, ez_, r1[3], r2[3];
+                int cx, cy, cz;
+                const bool more =
+                    vb_first_piece(wx.f0, wy.f0, wz.f0, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
+                deposit_seg<T>(jt, jbase, J, gorigin, g, wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx, ky, kz, scale);
+                if (more) {
+                    // the rest of a face-crossing path is deposited after the particle
+                    // loop, all queued paths together (keeps the loop convergent)
+                    const int jrem = jbase + cx + JPX * cy + JPY * cz;
+                    const unsigned slot = atomicAdd(qcount, 1u);
+                    if (slot < (unsigned)kQueue) {
+                        q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
+                        q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
+                        qcell[slot] = (unsigned)jrem;
                     } else {
-                        out.x[p] = x; out.y[p] = y; out.z[p] = z;
-                        atomicOr(err, (isfinite(xn) && isfinite(yn) && isfinite(zn)) ? kErrDisplacement
-                                                                                      : kErrNonFinite);
+                        deposit_remainder<T>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0], r2[1],
+                                             r2[2], kx, ky, kz, scale);
                     }
-                } else {
-                    push_outside_tile(g, EB, J, sp, x, y, z, ux, uy, uz, err);
-                    out.x[p] = x; out.y[p] = y; out.z[p] = z;
-                    out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
-                    u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
                 }
-                if (copy_id) out.id[p] = in.id[p];
+            } else {
+                atomicOr(err, (isfinite(xn) && isfinite(yn) && isfinite(zn)) ? kErrDisplacement
+                                                                              : kErrNonFinite);
             }
+        } else {
+            double xx = x, yy = y, zz = z;
+            push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+            out.x[p] = xx; out.y[p] = yy; out.z[p] = zz;
+            out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
+            u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
         }
-        __syncthreads();   // all particles of the supercell pushed, the queue is complete
-        // queued path remainders of this supercell
-        const int nq = min(*qcount, (unsigned)kQueue);
-        for (int e = tid; e < nq; e += kTileThreads) {
-            const int jrem = (int)qcell[e];
-            deposit_remainder<TJ, NJ>(jt, jrem, J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
-                                      q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz,
-                                      scale);
-        }
-        __syncthreads();
-        // flush the fixed-point tile to the fp64 global J and re-zero it
-        for (int t = tid; t < 3 * NJ; t += kTileThreads) {
-            const long long fx = (long long)(int)jt[6 * NJ + t] * 4294967296LL +
-                                 (long long)jt[3 * NJ + t] * 65536LL + (long long)jt[t];
-            if (fx != 0) {
-                const int comp = t / NJ, r = t - comp * NJ;
-                const int a = r % TJ, b = (r / TJ) % TJ, c = r / (TJ * TJ);
-                atomicAdd(J + comp * cs + gorigin + a + gsy * b + gsz * c, (double)fx * inv_scale);
-            }
-            jt[t] = 0u;   // chunk counters can be non-zero with a zero sum
-            jt[3 * NJ + t] = 0u;
-            jt[6 * NJ + t] = 0u;
-        }
-        if (tid == 0) *qcount = 0u;
-        __syncthreads();   // tile zeroed, E/B buffer (i & 1) free for the tile issued next iteration
-        sc = sc_nx;
+        if (copy_id) out.id[p] = in.id[p];
+        st ^= 1;
+    }
+    __syncthreads();   // all particles pushed, the remainder queue is complete
+    const int nq = min(*qcount, (unsigned)kQueue);
+    for (int e = tid; e < nq; e += NT) {
+        deposit_remainder<T>(jt, (int)qcell[e], J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
+                             q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz, scale);
+    }
+    __syncthreads();
+    // flush the fixed-point tile to the fp64 global J
+    const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
+    for (int t = tid; t < 3 * NJ; t += NT) {
+        const int comp = t / NJ, r = t - comp * NJ;
+        const int a = r % JPY % JPX, b = (r % JPY) / JPX, c = r / JPY;
+        if (a >= TJ || b >= TJ) continue;   // padding
+        const long long fx = (long long)(int)jt[6 * NJ + t] * 4294967296LL +
+                             (long long)jt[3 * NJ + t] * 65536LL + (long long)jt[t];
+        if (fx != 0)
+            atomicAdd(J + comp * cs + gorigin + a + gsy * b + gsz * c, (double)fx * inv_scale);
     }
     {
         const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc) >> 32));
@@ -390,20 +347,24 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 template <int S, int H>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
                         const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                        const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st)
+                        const SpeciesDev &sp, bool copy_id, unsigned *err, cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
-    const int nsc = g.nsx * g.nsy * g.nsz;
-    // persistent (kCtasPerSm per SM walking strided supercell lists) unless
-    // num_sms <= 0, which launches one CTA per supercell
-    const int grid = num_sms > 0 ? std::min(nsc, kCtasPerSm * num_sms) : nsc;
-    k_push_tile<S, H><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
-                                                        copy_id ? 1 : 0, err);
+    const int nsc = g.nsx * g.nsy * g.nsz;   // one CTA per supercell (empty ones exit at once)
+    k_push_tile<S, H><<<nsc, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
+                                                       copy_id ? 1 : 0, err);
 }
 
 bool tile_supported(int S) { return S == 2 || S == 4; }
 
-int tile_extent(int S) { return S + 2 * 1 + 2; }
+void tile_box(int S, int box[4])
+{
+    const int te = S + 2 * 1 + 2;
+    box[0] = (S == 4) ? TileGeom<4, 1>::EPX : TileGeom<2, 1>::EPX;
+    box[1] = te;
+    box[2] = te;
+    box[3] = 6;
+}
 
 void configure_tile_kernels()
 {
@@ -417,10 +378,11 @@ void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB
                       const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
                       const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st)
 {
+    (void)num_sms;
     if (g.S == 4)
-        launch_tile<4, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, num_sms, st);
+        launch_tile<4, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, st);
     else if (g.S == 2)
-        launch_tile<2, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, num_sms, st);
+        launch_tile<2, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, st);
 }
 
 }  // namespace pic

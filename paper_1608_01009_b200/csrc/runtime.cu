@@ -304,8 +304,9 @@ int build_graph(pic_ctx *ctx, bool sort_now, int jcur)
 }
 
 // TMA tensor map of the E/B fields: 4-D (x, y, z, component), box = one
-// supercell tile with halo (tile_extent^3 x 6), no swizzle, no OOB fill
-// (the ghost layers make every box in bounds).
+// supercell tile with halo (x extent padded to the shared row pitch) x 6,
+// no swizzle; box nodes past the padded array's x end are zero-filled and
+// never used.
 int encode_eb_map(pic_ctx *ctx)
 {
     void *fn = nullptr;
@@ -315,11 +316,12 @@ int encode_eb_map(pic_ctx *ctx)
         return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled unavailable");
     auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
     const GridDev &g = ctx->L.g;
-    const cuuint32_t te = (cuuint32_t)tile_extent(g.S);
+    int bx[4];
+    tile_box(g.S, bx);
     cuuint64_t dims[4] = {(cuuint64_t)g.X, (cuuint64_t)g.Y, (cuuint64_t)g.Z, 6};
     cuuint64_t strides[3] = {sizeof(double) * (cuuint64_t)g.X, sizeof(double) * (cuuint64_t)g.X * g.Y,
                              sizeof(double) * (cuuint64_t)g.cs};
-    cuuint32_t box[4] = {te, te, te, 6};
+    cuuint32_t box[4] = {(cuuint32_t)bx[0], (cuuint32_t)bx[1], (cuuint32_t)bx[2], (cuuint32_t)bx[3]};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode(&ctx->eb_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->EB, dims, strides, box,
                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
