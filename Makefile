@@ -3,8 +3,9 @@
 #   make sass       -> SASS dump of libpic.so into build/libpic.sass
 NVCC     ?= /usr/local/cuda/bin/nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
+NCCL_INC ?= $(shell python3 -c "import os,nvidia.nccl as m; print(os.path.join(list(m.__path__)[0],'include'))" 2>/dev/null || echo /usr/include)
 NVFLAGS  := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall \
-            -Xptxas -v -cudart static --expt-relaxed-constexpr
+            -Xptxas -v -cudart static --expt-relaxed-constexpr -I$(NCCL_INC)
 PKG      := paper_1608_01009_b200
 CSRC     := $(wildcard $(PKG)/csrc/*.cu)
 CHDR     := $(wildcard $(PKG)/csrc/*.cuh) include/pic.h
@@ -17,7 +18,7 @@ build/%.o: $(PKG)/csrc/%.cu $(CHDR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(PKG)/libpic.so: $(OBJ)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ) -ldl
 
 oracle/liboracle.so: oracle/pic_oracle.c oracle/pic_oracle.h
 	gcc -std=gnu11 -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm

@@ -107,6 +107,29 @@ def dist_env():
     return rank, world, local
 
 
+def reduce_max_over_ranks(v: float) -> float:
+    """max of a float over the initialised process group (identity without one)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(v)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum_over_ranks(v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(v)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
 def pinned_copy(P, ids):
     import torch
     tp = torch.empty(P.shape, dtype=torch.float64, pin_memory=True)
@@ -198,16 +221,20 @@ def run_ours(args, wl, rank, world, local):
     from synth import gen_particles
 
     torch.cuda.set_device(local)
+    nccl_id = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
-    parts = gen_particles(wl, rank=rank if world > 1 else None)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        nccl_id = pkg.broadcast_nccl_id(pkg.nccl_unique_id() if rank == 0 else bytes(128))
+        nzl = wl.nz // world
+        parts = gen_particles(wl, rank=rank, z_lo=rank * nzl, z_hi=(rank + 1) * nzl)
+    else:
+        parts = gen_particles(wl)
     n_local = sum(p.shape[1] for p, _ in parts)
 
     def new_sim(flags=0):
-        sim = pkg.simulation_from_workload(wl, capacity_factor=1.0, flags=flags,
-                                           rank=rank, nranks=world)
-        return sim
+        return pkg.simulation_from_workload(wl, capacity_factor=1.0, flags=flags, rank=rank,
+                                            nranks=world, nccl_id=nccl_id)
 
     def barrier():
         if world > 1:
@@ -230,18 +257,9 @@ def run_ours(args, wl, rank, world, local):
         e1.record(sim.stream)
         torch.cuda.synchronize()
         barrier()
-    t_ms = e0.elapsed_time(e1)
+    t_ms = reduce_max_over_ranks(e0.elapsed_time(e1))
     launches = sim.launch_count()
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([t_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
-        nt = torch.tensor([n_local], device="cuda", dtype=torch.float64)
-        dist.all_reduce(nt)
-        n_total = float(nt.item())
-    else:
-        n_total = float(n_local)
+    n_total = reduce_sum_over_ranks(float(n_local))
     value = n_total * args.steps / (t_ms * 1e-3)
     sim.close()
     del sim
@@ -295,12 +313,7 @@ def run_ours(args, wl, rank, world, local):
             esim.get_particles(s, out=outs[s])
         torch.cuda.synchronize()
         barrier()
-        te = time.perf_counter() - t0
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([te], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+        te = reduce_max_over_ranks(time.perf_counter() - t0)
         esim.close()
         bytes_io = n_local * 56.0
         e2e = {"value": n_total * args.steps / te, "unit": UNIT,

@@ -71,6 +71,8 @@ typedef struct pic_config {
     int64_t sort_every;                /* K: re-sort at the start of step n when n % K == 0 (0: never) */
     int64_t rank, nranks;              /* z-slab rank / count (1 for a single GPU) */
     int64_t flags;                     /* PIC_FLAG_* bits */
+    int64_t migrate_capacity;          /* nranks > 1: particles per species and direction that
+                                          may leave the slab in one step (0: default 65536) */
     uint8_t nccl_id[128];              /* ncclUniqueId from rank 0 (nranks > 1) */
     void *stream;                      /* cudaStream_t all work is enqueued on */
 } pic_config;
@@ -78,6 +80,9 @@ typedef struct pic_config {
 #define PIC_FLAG_NO_GRAPH 1   /* launch kernels directly instead of CUDA graphs */
 #define PIC_FLAG_PROFILE 2    /* record per-stage CUDA events (pic_get_stage_times) */
 #define PIC_FLAG_NAIVE 4      /* use the naive one-thread-per-particle kernel (tests) */
+#define PIC_FLAG_LOCAL_GROUP 8 /* nranks > 1 without NCCL: the slab contexts live in one
+                                  process on one device and are advanced together by
+                                  pic_step_group (single-GPU emulation of the z-slab path) */
 
 typedef struct pic_ctx pic_ctx;
 
@@ -114,13 +119,34 @@ int pic_set_fields(pic_ctx *ctx, const double *f);
  * PIC_ENONFINITE, PIC_ECAPACITY) if one was raised. */
 int pic_step(pic_ctx *ctx, int64_t nsteps);
 
+/* nranks > 1: z-slab decomposition.  Rank r owns the
+ * planes [r nz/nranks, (r+1) nz/nranks) (nz/nranks >= 4, divisible by S).
+ * Each step exchanges with ranks r-1 and r+1 (periodic ring), over NCCL
+ * point-to-point on cfg->stream: the J ghost planes (added by the owner), the
+ * particles whose z left the slab (fixed-capacity buffers, migrate_capacity
+ * per species and direction; overflow -> PIC_ECAPACITY), and the E and B
+ * ghost planes.  Received particles are pushed from an unsorted tail until
+ * the next sort.
+ *
+ * Writes the 128-byte ncclUniqueId that rank 0 distributes to all ranks (as
+ * cfg->nccl_id) before the collective pic_init.  PIC_ENCCL if NCCL cannot be
+ * loaded. */
+int pic_nccl_unique_id(uint8_t id[128]);
+
+/* Advances n slab contexts created with PIC_FLAG_LOCAL_GROUP (ranks 0..n-1 of
+ * one decomposition, same device and stream) by nsteps, exchanging ghost
+ * planes and particles with device-to-device copies instead of NCCL.  Same
+ * arithmetic and message layout as the NCCL path; used to check the
+ * decomposed step against the single-domain oracle on one GPU. */
+int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps);
+
 /* Copies E^n, B^n and J^{n-1/2} (the last deposit; zero before the first
  * step) of the local slab without ghosts into a HOST array
  * f[9][nz_local][ny][nx] (Ex,Ey,Ez,Bx,By,Bz,Jx,Jy,Jz). */
 int pic_get_fields(pic_ctx *ctx, double *f);
 
-/* Copies the particles of `species` in their current (sorted) device order
- * to HOST arrays.  *n_inout: capacity of the arrays in, particle count out
+/* Copies the live particles of `species` in their current device order
+ * (sorted region, then particles received since the last sort) to HOST arrays.  *n_inout: capacity of the arrays in, particle count out
  * (PIC_ECAPACITY, with the count written, when too small).  Positions are
  * wrapped into [0,L).  Any array pointer may be NULL to skip it. */
 int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout,

@@ -40,6 +40,8 @@ struct GridDev {
     int S;                   // supercell edge
     int nsx, nsy, nsz;       // supercells per axis (local)
     bool periodic_z_local;   // nranks == 1: z ghosts are local images
+    int nranks, rank;        // z slabs
+    double zlo, zhi;         // this rank's slab [zlo, zhi) in physical z
 };
 
 __host__ __device__ inline int64_t pidx(const GridDev &g, int i, int j, int k)
@@ -52,6 +54,19 @@ struct ParticlesDev {
     uint64_t *id;
 };
 
+// Particles that leave the slab (nranks > 1) go to a fixed-capacity send
+// buffer per direction: [0] = count (as double), then SoA x,y,z,ux,uy,uz,id
+// (id bits) with stride cap.  dir 0 = down (rank - 1), dir 1 = up (rank + 1).
+struct MigrateDev {
+    double *send[2];
+    unsigned *count;   // [2] running send counters
+    int cap;
+};
+
+// Dead slot marker: a particle that migrated away leaves x = -1 (live
+// positions are in [0, L)); kernels skip it, the next sort drops it.
+constexpr double kDeadX = -1.0;
+
 struct SpeciesDev {
     double qw;        // q * w
     double h;         // q dt / (2 m c)   (Boris half-kick coefficient)
@@ -60,6 +75,7 @@ struct SpeciesDev {
     // the fixed-point scale of the deposit tile (push_tile.cu).
     const unsigned *u2max_in;
     unsigned *u2max_out;
+    MigrateDev mig;
 };
 
 }  // namespace pic

@@ -35,11 +35,11 @@ __device__ __forceinline__ void for_images(const GridDev &g, int i, int j, int k
                 f(pidx(g, ii, jj, kk));
 }
 
-__global__ void __launch_bounds__(256) k_b_half(GridDev g, double *__restrict__ EB, double coef)
+__global__ void __launch_bounds__(256) k_b_half(GridDev g, double *__restrict__ EB, double coef, int kbegin)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
-    const int k = blockIdx.z;
+    const int k = blockIdx.z + kbegin;
     if (i >= g.nx || j >= g.ny) return;
     const int64_t cs = g.cs, sy = g.X, sz = (int64_t)g.X * g.Y;
     const double *Ex = EB, *Ey = EB + cs, *Ez = EB + 2 * cs;
@@ -119,10 +119,12 @@ static dim3 field_grid(const GridDev &g, dim3 bs)
     return dim3((g.nx + bs.x - 1) / bs.x, (g.ny + bs.y - 1) / bs.y, g.nz);
 }
 
-void launch_b_half(const GridDev &g, double *EB, cudaStream_t st)
+void launch_b_half(const GridDev &g, double *EB, cudaStream_t st, int kbegin)
 {
     const dim3 bs(32, 8, 1);
-    k_b_half<<<field_grid(g, bs), bs, 0, st>>>(g, EB, 0.5 * g.c * g.dt);
+    dim3 grid = field_grid(g, bs);
+    grid.z = g.nz - kbegin;
+    k_b_half<<<grid, bs, 0, st>>>(g, EB, 0.5 * g.c * g.dt, kbegin);
 }
 
 void launch_e_full(const GridDev &g, double *EB, double *Jcur, double *Jnext, cudaStream_t st)

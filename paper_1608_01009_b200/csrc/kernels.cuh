@@ -8,8 +8,9 @@
 namespace pic {
 
 // ---- fields.cu : Yee FDTD and ghost maintenance ----
-// B -= (c dt/2) curl E on the interior, result also stored to its ghost images.
-void launch_b_half(const GridDev &g, double *EB, cudaStream_t st);
+// B -= (c dt/2) curl E on planes [kbegin, nz) (kbegin = -1 computes the lower
+// z ghost plane of a slab locally), result also stored to its ghost images.
+void launch_b_half(const GridDev &g, double *EB, cudaStream_t st, int kbegin = 0);
 // E += c dt curl B - 4 pi dt J where J = sum of the ghost images of Jcur
 // (the fold); writes the folded J back into Jcur's interior,
 // stores E to its ghost images and zeroes every image of Jnext.
@@ -21,6 +22,11 @@ void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st)
 void launch_push_naive(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
                        const ParticlesDev &out, int64_t n, const SpeciesDev &sp, bool copy_id,
                        unsigned *err, cudaStream_t st);
+
+void launch_push_tail(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,
+                      const ParticlesDev &out, const int64_t *dev_lo, const int64_t *dev_hi,
+                      int64_t max_n, const SpeciesDev &sp, bool copy_id, unsigned *err,
+                      cudaStream_t st);
 
 // ---- push_tile.cu : fused supercell kernel ----
 bool tile_supported(int S);
@@ -43,10 +49,24 @@ struct SortScratch {
     uint32_t *block_sums;// [scan blocks]
 };
 size_t scan_block_count(int64_t nitems);
-// Sorts n particles src -> dst (x,y,z,ux,uy,uz,id) and writes the supercell
-// offsets sc_off[0..n_sc] (int64).
-void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst, int64_t n,
-                    const SortScratch &s, int64_t *sc_off, unsigned *err, cudaStream_t st,
-                    int *launches);
+// Sorts the *dev_n particle slots src -> dst (x,y,z,ux,uy,uz,id), dropping
+// dead slots (x == kDeadX); writes the supercell offsets sc_off[0..n_sc]
+// (int64) and the live count back to *dev_n.  Grids are sized for cap.
+void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst,
+                    int64_t *dev_n, int64_t cap, const SortScratch &s, int64_t *sc_off,
+                    unsigned *err, cudaStream_t st, int *launches);
+
+// ---- slab.cu : z-slab exchange helpers ----
+// J ghost planes received from the neighbours are added into the interior
+// planes they belong to; this rank's own J ghost planes (already sent) are
+// zeroed for the next deposit.  recv_dn: from rank-1 (its planes nz, nz+1 =
+// our 0, 1); recv_up: from rank+1 (its planes -2, -1 = our nz-2, nz-1).
+void launch_j_ghost_add(const GridDev &g, double *J, const double *recv_dn, const double *recv_up,
+                        cudaStream_t st);
+// header (count, capped) of a migration send buffer, capacity check
+void launch_mig_finalize(const MigrateDev &m, unsigned *err, cudaStream_t st);
+// appends the particles of two received migration buffers at the tail of P
+void launch_mig_append(const double *recv0, const double *recv1, int cap, const ParticlesDev &P,
+                       int64_t *dev_n, int64_t pcap, unsigned *err, cudaStream_t st);
 
 }  // namespace pic

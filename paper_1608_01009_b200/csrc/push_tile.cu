@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "particle_store.cuh"
 #include "push_global.cuh"
 #include "tma.cuh"
 
@@ -240,7 +241,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         cp_async_commit();
         cp_async_wait1();
         const double *pl = pbuf + st * 6 * NT + tid;
+        st ^= 1;
         const double x = pl[0], y = pl[NT], z = pl[2 * NT];
+        if (x < 0.0) continue;   // dead slot (migrated away since the last sort)
         double ux = pl[3 * NT], uy = pl[4 * NT], uz = pl[5 * NT];
         const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
         const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
@@ -265,11 +268,12 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double byl = yn * g.inv_dy - (double)wy.i0;
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
             const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
-            out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
-            out.x[p] = ok ? wrap_coord(xn, g.Lx) : x;
-            out.y[p] = ok ? wrap_coord(yn, g.Ly) : y;
-            out.z[p] = ok ? wrap_coord(zn, g.Lz) : z;
             u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+            if (ok)
+                store_particle(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
+                               wrap_coord(zn, g.Lz), ux, uy, uz, copy_id != 0, err);
+            else
+                store_particle(g, sp, out, in.id, p, x, y, z, ux, uy, uz, copy_id != 0, err);
             if (ok) {
                 const int jbase = tx + JPX * ty + JPY * tz;
                 double ex_, ey_, ez_, r1[3], r2[3];
@@ -298,12 +302,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         } else {
             double xx = x, yy = y, zz = z;
             push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
-            out.x[p] = xx; out.y[p] = yy; out.z[p] = zz;
-            out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
+            store_particle(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
             u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
         }
-        if (copy_id) out.id[p] = in.id[p];
-        st ^= 1;
     }
     __syncthreads();   // all particles pushed, the remainder queue is complete
     const int nq = min(*qcount, (unsigned)kQueue);

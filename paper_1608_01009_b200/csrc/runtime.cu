@@ -1,24 +1,34 @@
 // runtime.cu -- the C ABI of libpic.so (include/pic.h): validation,
-// workspace carving, the per-step launch schedule, CUDA graph capture,
-// stage timing and the sticky device error word.
+// workspace carving, the per-step schedule, CUDA graph capture, the z-slab
+// exchanges (NCCL or in-process device copies), stage timing and the sticky
+// device error word.
 //
 // Per step n:
-//   a1  n % K == 0: stable sort A -> B per species (sort.cu)
-//   a2-a6 particle kernel per species, input B on a sort step else A,
-//       output A (in place), deposit into J_cur
-//   a7  B half, E full (+ J fold, zero J_next), B half (fields.cu)
-//   swap J_cur / J_next
+//   A  a1   n % K == 0: sort A -> B per species (sort.cu), dropping dead slots
+//      a2-6 fused particle kernel per species (input B on a sort step else A,
+//           output A in place), deposit into J_cur; [slabs] tail kernel for
+//           particles received since the last sort; migration headers
+//   X1 [slabs] J ghost planes + migrating particles to ranks r-1, r+1
+//   B  [slabs] add received J planes, append received particles;
+//      a7   B half (from plane -1 on slabs), E full (+ J fold, zero J_next)
+//   X2 [slabs] E ghost planes
+//   C  a7   B half
+//   X3 [slabs] B ghost planes
+//   then swap J_cur / J_next.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
-#include <mutex>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "../../include/pic.h"
 #include "kernels.cuh"
@@ -29,15 +39,19 @@ namespace {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+constexpr int64_t kDefaultMigrate = 65536;
 
 struct Layout {
     GridDev g{};
     int64_t ncells = 0, n_sc = 0;
     int64_t cap[PIC_MAX_SPECIES] = {};
     int64_t cap_max = 0;
+    int64_t mig = 0;   // migration capacity (per species and direction), 0 on one rank
     size_t off_eb = 0, off_j[2] = {}, off_sp[PIC_MAX_SPECIES][2] = {}, off_scoff[PIC_MAX_SPECIES] = {};
     size_t off_key = 0, off_slot = 0, off_perm_tmp = 0, off_perm = 0, off_count = 0, off_start = 0,
-           off_bsums = 0, off_err = 0, off_stat = 0;
+           off_bsums = 0, off_err = 0, off_stat = 0, off_n = 0;
+    size_t off_msend[PIC_MAX_SPECIES][2] = {}, off_mrecv[PIC_MAX_SPECIES][2] = {}, off_mcnt = 0;
+    size_t off_jrecv[2] = {};
     size_t total = 0;
 };
 
@@ -62,9 +76,10 @@ std::string validate(const pic_config *c)
     const int64_t nzl = c->nz / c->nranks;
     if (c->nx % c->supercell || c->ny % c->supercell || nzl % c->supercell)
         return "supercell must divide nx, ny and nz/nranks";
+    if (c->nranks > 1 && nzl < 4) return "z slabs must be at least 4 cells thick";
     if (c->sort_every < 0) return "sort_every must be >= 0";
+    if (c->migrate_capacity < 0 || c->migrate_capacity >= (int64_t(1) << 28)) return "bad migrate_capacity";
     if (c->nx * c->ny * nzl >= (int64_t(1) << 31)) return "local grid too large";
-    if (c->nranks > 1) return "nranks > 1: z-slab exchange not built in this version";
     return "";
 }
 
@@ -78,7 +93,7 @@ Layout make_layout(const pic_config *c)
     g.nz_global = (int)c->nz;
     g.k0 = (int)(c->rank * g.nz);
     g.X = g.nx + 2 * kGhost;
-    g.X += g.X & 1;   // 16-byte row pitch
+    g.X += g.X & 1;   // 16-byte row pitch (TMA global strides)
     g.Y = g.ny + 2 * kGhost;
     g.Z = g.nz + 2 * kGhost;
     g.cs = (int64_t)g.X * g.Y * g.Z;
@@ -90,8 +105,13 @@ Layout make_layout(const pic_config *c)
     g.S = (int)c->supercell;
     g.nsx = g.nx / g.S; g.nsy = g.ny / g.S; g.nsz = g.nz / g.S;
     g.periodic_z_local = (c->nranks == 1);
+    g.nranks = (int)c->nranks;
+    g.rank = (int)c->rank;
+    g.zlo = c->nranks == 1 ? 0.0 : (double)g.k0 * c->dz;
+    g.zhi = c->nranks == 1 ? g.Lz : (c->rank == c->nranks - 1 ? g.Lz : (double)(g.k0 + g.nz) * c->dz);
     L.ncells = (int64_t)g.nx * g.ny * g.nz;
     L.n_sc = (int64_t)g.nsx * g.nsy * g.nsz;
+    L.mig = c->nranks > 1 ? (c->migrate_capacity ? c->migrate_capacity : kDefaultMigrate) : 0;
     size_t o = 0;
     L.off_eb = o; o = align_up(o + sizeof(double) * 6 * (size_t)g.cs);
     for (int b = 0; b < 2; ++b) { L.off_j[b] = o; o = align_up(o + sizeof(double) * 3 * (size_t)g.cs); }
@@ -100,9 +120,21 @@ Layout make_layout(const pic_config *c)
         L.cap_max = std::max(L.cap_max, L.cap[s]);
         for (int b = 0; b < 2; ++b) {
             L.off_sp[s][b] = o;
-            o = align_up(o + (sizeof(double) * 6 + sizeof(uint64_t)) * (size_t)L.cap[s] + 6 * kAlign);
+            o = align_up(o + (sizeof(double) * 6 + sizeof(uint64_t)) * (size_t)L.cap[s] + 8 * kAlign);
         }
         L.off_scoff[s] = o; o = align_up(o + sizeof(int64_t) * (size_t)(L.n_sc + 1));
+        if (L.mig) {
+            for (int d = 0; d < 2; ++d) {
+                L.off_msend[s][d] = o; o = align_up(o + sizeof(double) * (size_t)(1 + 7 * L.mig));
+                L.off_mrecv[s][d] = o; o = align_up(o + sizeof(double) * (size_t)(1 + 7 * L.mig));
+            }
+        }
+    }
+    if (L.mig) {
+        for (int d = 0; d < 2; ++d) {
+            L.off_jrecv[d] = o;
+            o = align_up(o + sizeof(double) * 3 * 2 * (size_t)g.X * g.Y);
+        }
     }
     const size_t capm = (size_t)std::max<int64_t>(L.cap_max, 1);
     L.off_key = o; o = align_up(o + 4 * capm);
@@ -114,6 +146,8 @@ Layout make_layout(const pic_config *c)
     L.off_bsums = o; o = align_up(o + 4 * scan_block_count(L.ncells + 1));
     L.off_err = o; o = align_up(o + 64);
     L.off_stat = o; o = align_up(o + 2 * PIC_MAX_SPECIES * sizeof(unsigned));
+    L.off_n = o; o = align_up(o + PIC_MAX_SPECIES * sizeof(int64_t));
+    L.off_mcnt = o; o = align_up(o + 2 * PIC_MAX_SPECIES * sizeof(unsigned));
     L.total = o;
     return L;
 }
@@ -121,7 +155,7 @@ Layout make_layout(const pic_config *c)
 ParticlesDev carve_particles(char *base, size_t off, int64_t cap)
 {
     ParticlesDev p;
-    const size_t col = align_up(sizeof(double) * (size_t)cap);
+    const size_t col = align_up(sizeof(double) * (size_t)cap + 16);   // +16: a chunk may read 1 past
     char *b = base + off;
     p.x = (double *)(b + 0 * col);
     p.y = (double *)(b + 1 * col);
@@ -149,6 +183,58 @@ const char *err_names(int code)
     }
 }
 
+// ---- NCCL, loaded at run time (only z-slab runs need it): the copy torch
+// already loaded if any, else the torch wheel's, else the system's ----
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char *(*errorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi *nccl_api()
+{
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api.h ? &api : nullptr;
+    tried = true;
+    const char *names[] = {"libnccl.so.2",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
+                           "libnccl.so"};
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    for (const char *n : names)
+        if (!h) h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return nullptr;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.send = (decltype(api.send))dlsym(h, "ncclSend");
+    api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+    api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+    api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+    if (!api.getUniqueId || !api.commInitRank || !api.send || !api.recv || !api.groupStart ||
+        !api.groupEnd || !api.commDestroy)
+        return nullptr;
+    api.h = h;
+    return &api;
+}
+
+// one point-to-point message of an exchange: every rank sends `send` toward
+// dir (0 = rank-1, 1 = rank+1) and receives the same message of the rank on
+// the other side into `recv`
+struct Msg {
+    double *send;
+    double *recv;
+    size_t count;
+    int dir;
+};
+
 }  // namespace
 
 struct pic_ctx {
@@ -162,14 +248,22 @@ struct pic_ctx {
     int jlast = 1;             // J buffer holding J^{n-1/2}
     ParticlesDev A[PIC_MAX_SPECIES], B[PIC_MAX_SPECIES];
     int64_t *sc_off[PIC_MAX_SPECIES] = {};
-    int64_t count[PIC_MAX_SPECIES] = {};
+    int64_t *dev_n = nullptr;  // [species] particle slots in use (sorted region + tail)
+    bool has_particles[PIC_MAX_SPECIES] = {};
     SortScratch sort{};
     unsigned *err = nullptr;
     unsigned *u2max[2] = {nullptr, nullptr};   // [parity][species], see SpeciesDev
+    MigrateDev mig[PIC_MAX_SPECIES];
+    double *mrecv[PIC_MAX_SPECIES][2] = {};
+    double *jrecv[2] = {nullptr, nullptr};     // [from rank-1, from rank+1]
     int64_t step_index = 0;
     bool use_tile = false;     // fused supercell kernel (else the naive kernel)
+    bool slabs = false;        // nranks > 1
+    bool local_group = false;  // slabs exchanged by pic_step_group (no NCCL)
+    bool ghosts_stale = false; // E/B z ghosts need an exchange (after pic_set_fields)
     CUtensorMap eb_map;        // TMA descriptor of the padded E/B array [6][Z][Y][X]
     int num_sms = 148;
+    ncclComm_t comm = nullptr;
     std::string last_error;
     // graphs keyed by (sort_now, jcur)
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -234,8 +328,92 @@ struct StageMark {
     }
 };
 
-// Enqueue one full step; returns the number of kernel launches enqueued.
-int enqueue_step(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
+SpeciesDev species_dev(pic_ctx *ctx, int s, int jcur)
+{
+    const GridDev &g = ctx->L.g;
+    SpeciesDev sp;
+    sp.qw = ctx->cfg.q[s] * ctx->cfg.w[s];
+    sp.h = ctx->cfg.q[s] * g.dt / (2.0 * ctx->cfg.m[s] * g.c);
+    sp.u2max_in = ctx->u2max[jcur] + s;
+    sp.u2max_out = ctx->u2max[1 - jcur] + s;
+    sp.mig = ctx->mig[s];
+    return sp;
+}
+
+// ---- exchanges (slabs) ----
+size_t plane_pair(const GridDev &g) { return 2 * (size_t)g.X * g.Y; }
+// padded-array offset of local plane k (first of the pair) within one component
+size_t plane_off(const GridDev &g, int k) { return (size_t)(k + kGhost) * g.X * g.Y; }
+
+std::vector<Msg> msgs_fields(pic_ctx *ctx, int c0, int c1)
+{
+    // send own boundary planes {0,1} down and {nz-2,nz-1} up; receive into the
+    // ghost planes {nz, nz+1} (from rank+1) and {-2,-1} (from rank-1)
+    const GridDev &g = ctx->L.g;
+    std::vector<Msg> m;
+    for (int c = c0; c < c1; ++c) {
+        double *F = ctx->EB + c * g.cs;
+        m.push_back({F + plane_off(g, 0), F + plane_off(g, g.nz), plane_pair(g), 0});
+        m.push_back({F + plane_off(g, g.nz - 2), F + plane_off(g, -2), plane_pair(g), 1});
+    }
+    return m;
+}
+
+std::vector<Msg> msgs_current(pic_ctx *ctx, int jcur)
+{
+    // own J ghost planes {-2,-1} go down, {nz,nz+1} go up; the neighbours'
+    // arrive in jrecv[1] (from rank+1) and jrecv[0] (from rank-1)
+    const GridDev &g = ctx->L.g;
+    std::vector<Msg> m;
+    for (int c = 0; c < 3; ++c) {
+        double *Jc = ctx->J[jcur] + c * g.cs;
+        m.push_back({Jc + plane_off(g, -2), ctx->jrecv[1] + c * plane_pair(g), plane_pair(g), 0});
+        m.push_back({Jc + plane_off(g, g.nz), ctx->jrecv[0] + c * plane_pair(g), plane_pair(g), 1});
+    }
+    for (int s = 0; s < ctx->cfg.n_species; ++s) {
+        const size_t n = 1 + 7 * (size_t)ctx->L.mig;
+        m.push_back({ctx->mig[s].send[0], ctx->mrecv[s][1], n, 0});
+        m.push_back({ctx->mig[s].send[1], ctx->mrecv[s][0], n, 1});
+    }
+    return m;
+}
+
+int exchange_nccl(pic_ctx *ctx, const std::vector<Msg> &msgs)
+{
+    NcclApi *api = nccl_api();
+    if (!api || !ctx->comm) return fail(ctx, PIC_ENCCL, "NCCL not initialised");
+    const int r = (int)ctx->cfg.rank, n = (int)ctx->cfg.nranks;
+    const int dn = (r + n - 1) % n, up = (r + 1) % n;
+    ncclResult_t e = api->groupStart();
+    // sends and receives are each posted in message order, so with two ranks
+    // (dn == up) the i-th send matches the peer's i-th receive
+    for (const Msg &m : msgs)
+        if (e == ncclSuccess) e = api->send(m.send, m.count, ncclFloat64, m.dir == 0 ? dn : up, ctx->comm, ctx->st);
+    for (const Msg &m : msgs)
+        if (e == ncclSuccess) e = api->recv(m.recv, m.count, ncclFloat64, m.dir == 0 ? up : dn, ctx->comm, ctx->st);
+    const ncclResult_t e2 = api->groupEnd();
+    if (e != ncclSuccess || e2 != ncclSuccess)
+        return fail(ctx, PIC_ENCCL, std::string("NCCL exchange: ") +
+                                        (api->errorString ? api->errorString(e != ncclSuccess ? e : e2) : ""));
+    return PIC_OK;
+}
+
+// copies message i of every rank into its receiver (in-process slab group)
+int exchange_local(pic_ctx *const *ctxs, int n, const std::vector<std::vector<Msg>> &msgs)
+{
+    for (int r = 0; r < n; ++r) {
+        for (size_t i = 0; i < msgs[r].size(); ++i) {
+            const Msg &m = msgs[r][i];
+            const int src = m.dir == 0 ? (r + 1) % n : (r + n - 1) % n;   // who sends toward r
+            PIC_CUDA(ctxs[r], cudaMemcpyAsync(m.recv, msgs[src][i].send, m.count * sizeof(double),
+                                              cudaMemcpyDeviceToDevice, ctxs[r]->st));
+        }
+    }
+    return PIC_OK;
+}
+
+// ---- the phases of one step; each returns the number of kernel launches ----
+int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
 {
     const Layout &L = ctx->L;
     const GridDev &g = L.g;
@@ -243,38 +421,85 @@ int enqueue_step(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
     if (sort_now) {
         StageMark m(ctx, 0, profile);
         for (int s = 0; s < ctx->cfg.n_species; ++s)
-            sort_particles(g, ctx->A[s], ctx->B[s], ctx->count[s], ctx->sort, ctx->sc_off[s],
-                           ctx->err, ctx->st, &launches);
+            if (ctx->has_particles[s])
+                sort_particles(g, ctx->A[s], ctx->B[s], ctx->dev_n + s, L.cap[s], ctx->sort, ctx->sc_off[s],
+                               ctx->err, ctx->st, &launches);
     }
-    {
-        StageMark m(ctx, 1, profile);
-        // u^2 bounds: this step reads parity jcur, writes parity 1 - jcur
-        cudaMemsetAsync(ctx->u2max[1 - jcur], 0, PIC_MAX_SPECIES * sizeof(unsigned), ctx->st);
-        for (int s = 0; s < ctx->cfg.n_species; ++s) {
-            if (ctx->count[s] == 0) continue;
-            SpeciesDev sp;
-            sp.qw = ctx->cfg.q[s] * ctx->cfg.w[s];
-            sp.h = ctx->cfg.q[s] * g.dt / (2.0 * ctx->cfg.m[s] * g.c);
-            sp.u2max_in = ctx->u2max[jcur] + s;
-            sp.u2max_out = ctx->u2max[1 - jcur] + s;
-            const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
-            if (ctx->use_tile)
-                launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s],
-                                 sp, sort_now, ctx->err, ctx->num_sms, ctx->st);
-            else
-                launch_push_naive(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->count[s], sp,
-                                  sort_now, ctx->err, ctx->st);
+    StageMark m(ctx, 1, profile);
+    // u^2 bounds: this step reads parity jcur, writes parity 1 - jcur
+    cudaMemsetAsync(ctx->u2max[1 - jcur], 0, PIC_MAX_SPECIES * sizeof(unsigned), ctx->st);
+    for (int s = 0; s < ctx->cfg.n_species; ++s) {
+        if (!ctx->has_particles[s]) continue;
+        const SpeciesDev sp = species_dev(ctx, s, jcur);
+        const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
+        if (ctx->use_tile)
+            launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s], sp,
+                             sort_now, ctx->err, ctx->num_sms, ctx->st);
+        else
+            launch_push_tail(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], nullptr, ctx->dev_n + s, L.cap[s], sp,
+                             sort_now, ctx->err, ctx->st);
+        ++launches;
+        if (profile) ctx->particle_launches++;
+        if (ctx->slabs) {
+            if (ctx->use_tile) {   // particles received since the last sort (none right after it)
+                if (!sort_now) {
+                    launch_push_tail(g, ctx->EB, ctx->J[jcur], ctx->A[s], ctx->A[s], ctx->sc_off[s] + L.n_sc,
+                                     ctx->dev_n + s, 4 * L.mig, sp, false, ctx->err, ctx->st);
+                    ++launches;
+                }
+            }
+            launch_mig_finalize(ctx->mig[s], ctx->err, ctx->st);
             ++launches;
-            if (profile) ctx->particle_launches++;
         }
     }
-    {
-        StageMark m(ctx, 2, profile);
-        launch_b_half(g, ctx->EB, ctx->st);
-        launch_e_full(g, ctx->EB, ctx->J[jcur], ctx->J[1 - jcur], ctx->st);
-        launch_b_half(g, ctx->EB, ctx->st);
-        launches += 3;
+    return launches;
+}
+
+int phase_fields_e(pic_ctx *ctx, int jcur, bool profile)
+{
+    const GridDev &g = ctx->L.g;
+    StageMark m(ctx, 2, profile);
+    int launches = 0;
+    if (ctx->slabs) {
+        launch_j_ghost_add(g, ctx->J[jcur], ctx->jrecv[0], ctx->jrecv[1], ctx->st);
+        ++launches;
+        for (int s = 0; s < ctx->cfg.n_species; ++s) {
+            launch_mig_append(ctx->mrecv[s][0], ctx->mrecv[s][1], (int)ctx->L.mig, ctx->A[s], ctx->dev_n + s,
+                              ctx->L.cap[s], ctx->err, ctx->st);
+            launches += 2;
+        }
     }
+    launch_b_half(g, ctx->EB, ctx->st, ctx->slabs ? -1 : 0);
+    launch_e_full(g, ctx->EB, ctx->J[jcur], ctx->J[1 - jcur], ctx->st);
+    return launches + 2;
+}
+
+int phase_fields_b(pic_ctx *ctx, bool profile)
+{
+    StageMark m(ctx, 2, profile);
+    launch_b_half(ctx->L.g, ctx->EB, ctx->st, 0);
+    return 1;
+}
+
+// a whole step on one rank (NCCL exchanges or none); returns launches or < 0
+int enqueue_step(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
+{
+    int launches = phase_push(ctx, sort_now, jcur, profile);
+    if (ctx->slabs) {
+        StageMark m(ctx, 3, profile);
+        if (exchange_nccl(ctx, msgs_current(ctx, jcur)) != PIC_OK) return -1;
+    }
+    launches += phase_fields_e(ctx, jcur, profile);
+    if (ctx->slabs) {
+        StageMark m(ctx, 3, profile);
+        if (exchange_nccl(ctx, msgs_fields(ctx, 0, 3)) != PIC_OK) return -1;
+    }
+    launches += phase_fields_b(ctx, profile);
+    if (ctx->slabs) {
+        StageMark m(ctx, 3, profile);
+        if (exchange_nccl(ctx, msgs_fields(ctx, 3, 6)) != PIC_OK) return -1;
+    }
+    for (int s = 0; s < ctx->cfg.n_species; ++s) ctx->has_particles[s] = ctx->has_particles[s] || ctx->slabs;
     return launches;
 }
 
@@ -295,6 +520,10 @@ int build_graph(pic_ctx *ctx, bool sort_now, int jcur)
     PIC_CUDA(ctx, cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     const int n = enqueue_step(ctx, sort_now, jcur, false);
     cudaError_t e = cudaStreamEndCapture(ctx->st, &graph);
+    if (n < 0) {
+        if (e == cudaSuccess) cudaGraphDestroy(graph);
+        return PIC_ENCCL;
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
     e = cudaGraphInstantiate(&ctx->graph[sort_now][jcur], graph, 0);
     cudaGraphDestroy(graph);
@@ -337,9 +566,20 @@ int check_device_error(pic_ctx *ctx)
     PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     if (h & kErrNonFinite) return fail(ctx, PIC_ENONFINITE, "non-finite particle state");
     if (h & kErrDisplacement) return fail(ctx, PIC_EDISPLACEMENT, "displacement >= 1 cell");
-    if (h & kErrRange) return fail(ctx, PIC_EINVAL, "particle position outside the domain");
-    if (h & kErrCapacity) return fail(ctx, PIC_ECAPACITY, "device capacity exceeded");
+    if (h & kErrRange) return fail(ctx, PIC_EINVAL, "particle position outside the domain / slab");
+    if (h & kErrCapacity) return fail(ctx, PIC_ECAPACITY, "device capacity exceeded (particles or migration)");
     return PIC_OK;
+}
+
+void collect_profile(pic_ctx *ctx)
+{
+    for (auto &m : ctx->ev_marks) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+        ctx->stage_ms[m.first] += ms;
+    }
+    ctx->ev_marks.clear();
+    ctx->ev_used = 0;
 }
 
 }  // namespace
@@ -351,6 +591,18 @@ int pic_workspace_size(const pic_config *cfg, size_t *bytes)
     const std::string v = validate(cfg);
     if (!v.empty() || !bytes) return PIC_EINVAL;
     *bytes = make_layout(cfg).total;
+    return PIC_OK;
+}
+
+int pic_nccl_unique_id(uint8_t id[128])
+{
+    if (!id) return PIC_EINVAL;
+    NcclApi *api = nccl_api();
+    if (!api) return PIC_ENCCL;
+    ncclUniqueId u;
+    if (api->getUniqueId(&u) != ncclSuccess) return PIC_ENCCL;
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    memcpy(id, &u, 128);
     return PIC_OK;
 }
 
@@ -370,14 +622,27 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->L = L;
     ctx->ws = (char *)d_workspace;
     ctx->st = (cudaStream_t)cfg->stream;
+    ctx->slabs = cfg->nranks > 1;
+    ctx->local_group = ctx->slabs && (cfg->flags & PIC_FLAG_LOCAL_GROUP);
     ctx->EB = (double *)(ctx->ws + L.off_eb);
     ctx->J[0] = (double *)(ctx->ws + L.off_j[0]);
     ctx->J[1] = (double *)(ctx->ws + L.off_j[1]);
+    ctx->u2max[0] = (unsigned *)(ctx->ws + L.off_stat);
+    ctx->u2max[1] = ctx->u2max[0] + PIC_MAX_SPECIES;
+    ctx->dev_n = (int64_t *)(ctx->ws + L.off_n);
+    unsigned *mcnt = (unsigned *)(ctx->ws + L.off_mcnt);
     for (int s = 0; s < cfg->n_species; ++s) {
         ctx->A[s] = carve_particles(ctx->ws, L.off_sp[s][0], L.cap[s]);
         ctx->B[s] = carve_particles(ctx->ws, L.off_sp[s][1], L.cap[s]);
         ctx->sc_off[s] = (int64_t *)(ctx->ws + L.off_scoff[s]);
+        ctx->mig[s].cap = (int)L.mig;
+        ctx->mig[s].count = mcnt + 2 * s;
+        for (int d = 0; d < 2; ++d) {
+            ctx->mig[s].send[d] = L.mig ? (double *)(ctx->ws + L.off_msend[s][d]) : nullptr;
+            ctx->mrecv[s][d] = L.mig ? (double *)(ctx->ws + L.off_mrecv[s][d]) : nullptr;
+        }
     }
+    for (int d = 0; d < 2; ++d) ctx->jrecv[d] = L.mig ? (double *)(ctx->ws + L.off_jrecv[d]) : nullptr;
     ctx->sort.key = (uint32_t *)(ctx->ws + L.off_key);
     ctx->sort.slot = (uint32_t *)(ctx->ws + L.off_slot);
     ctx->sort.perm_tmp = (uint32_t *)(ctx->ws + L.off_perm_tmp);
@@ -386,31 +651,36 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->sort.start = (uint32_t *)(ctx->ws + L.off_start);
     ctx->sort.block_sums = (uint32_t *)(ctx->ws + L.off_bsums);
     ctx->err = (unsigned *)(ctx->ws + L.off_err);
-    ctx->u2max[0] = (unsigned *)(ctx->ws + L.off_stat);
-    ctx->u2max[1] = ctx->u2max[0] + PIC_MAX_SPECIES;
     ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell);
     configure_tile_kernels();
     {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
-        const char *pe = getenv("PIC_TILE_PERSISTENT");   // tuning knob: "0" = one CTA per supercell
-        if (pe && pe[0] == '0') ctx->num_sms = 0;
     }
     if (ctx->use_tile && encode_eb_map(ctx) != PIC_OK) {
         delete ctx;
         return PIC_ECUDA;
     }
-    // zero fields, offsets and the error word (particle arrays stay garbage until set)
+    // zero fields, offsets, counters and the error word (particle arrays stay
+    // garbage until set; the exchange buffers are written before being read)
     cudaError_t e = cudaMemsetAsync(ctx->ws, 0, L.off_sp[0][0], ctx->st);
     for (int s = 0; e == cudaSuccess && s < cfg->n_species; ++s)
         e = cudaMemsetAsync(ctx->sc_off[s], 0, sizeof(int64_t) * (size_t)(L.n_sc + 1), ctx->st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->err, 0, 64, ctx->st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->u2max[0], 0, 2 * PIC_MAX_SPECIES * sizeof(unsigned), ctx->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->ws + L.off_err, 0, L.total - L.off_err, ctx->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
     if (e != cudaSuccess) {
         delete ctx;
         return PIC_ECUDA;
+    }
+    if (ctx->slabs && !ctx->local_group) {
+        NcclApi *api = nccl_api();
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_id, 128);
+        if (!api || api->commInitRank(&ctx->comm, (int)cfg->nranks, id, (int)cfg->rank) != ncclSuccess) {
+            delete ctx;
+            return PIC_ENCCL;
+        }
     }
     *out = ctx;
     return PIC_OK;
@@ -424,27 +694,40 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
     if (species < 0 || species >= ctx->cfg.n_species) return fail(ctx, PIC_EINVAL, "bad species");
     if (n < 0 || (n > 0 && !(x && y && z && ux && uy && uz && id)))
         return fail(ctx, PIC_EINVAL, "bad particle arrays");
-    if (n > ctx->L.cap[species]) return fail(ctx, PIC_ECAPACITY, "n exceeds capacity");
     const GridDev &g = ctx->L.g;
     for (int64_t p = 0; p < n; ++p) {
         if (!(x[p] >= 0.0 && x[p] < g.Lx && y[p] >= 0.0 && y[p] < g.Ly && z[p] >= 0.0 && z[p] < g.Lz))
             return fail(ctx, PIC_EINVAL, "particle position outside [0, L)");
     }
-    const ParticlesDev &Bs = ctx->B[species];
-    const size_t bytes = sizeof(double) * (size_t)n;
     const double *src[6] = {x, y, z, ux, uy, uz};
+    std::vector<double> sel[6];
+    std::vector<uint64_t> sel_id;
+    int64_t m = n;
+    if (ctx->slabs) {   // keep the particles of this rank's slab
+        for (int c = 0; c < 6; ++c) sel[c].reserve((size_t)(n / ctx->cfg.nranks + 16));
+        for (int64_t p = 0; p < n; ++p)
+            if (z[p] >= g.zlo && z[p] < g.zhi) {
+                for (int c = 0; c < 6; ++c) sel[c].push_back(src[c][p]);
+                sel_id.push_back(id[p]);
+            }
+        m = (int64_t)sel_id.size();
+        for (int c = 0; c < 6; ++c) src[c] = sel[c].data();
+        id = sel_id.data();
+    }
+    if (m > ctx->L.cap[species]) return fail(ctx, PIC_ECAPACITY, "n exceeds capacity");
+    const ParticlesDev &Bs = ctx->B[species];
     double *dst[6] = {Bs.x, Bs.y, Bs.z, Bs.ux, Bs.uy, Bs.uz};
-    for (int c = 0; c < 6 && n > 0; ++c)
-        PIC_CUDA(ctx, cudaMemcpyAsync(dst[c], src[c], bytes, cudaMemcpyHostToDevice, ctx->st));
-    if (n > 0)
-        PIC_CUDA(ctx, cudaMemcpyAsync(Bs.id, id, sizeof(uint64_t) * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
-    ctx->count[species] = n;
+    for (int c = 0; c < 6 && m > 0; ++c)
+        PIC_CUDA(ctx, cudaMemcpyAsync(dst[c], src[c], sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, ctx->st));
+    if (m > 0)
+        PIC_CUDA(ctx, cudaMemcpyAsync(Bs.id, id, sizeof(uint64_t) * (size_t)m, cudaMemcpyHostToDevice, ctx->st));
+    PIC_CUDA(ctx, cudaMemcpyAsync(ctx->dev_n + species, &m, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->st));
+    ctx->has_particles[species] = m > 0 || ctx->slabs;
     int launches = 0;
-    sort_particles(g, Bs, ctx->A[species], n, ctx->sort, ctx->sc_off[species], ctx->err, ctx->st,
-                   &launches);
-    launch_u2max(ctx->A[species], n, ctx->u2max[ctx->jcur] + species, ctx->st);
-    ++launches;
-    ctx->launches += launches;
+    sort_particles(g, Bs, ctx->A[species], ctx->dev_n + species, std::max<int64_t>(m, 1), ctx->sort,
+                   ctx->sc_off[species], ctx->err, ctx->st, &launches);
+    launch_u2max(ctx->A[species], m, ctx->u2max[ctx->jcur] + species, ctx->st);
+    ctx->launches += launches + 1;
     PIC_CUDA(ctx, cudaGetLastError());
     destroy_graphs(ctx);
     return check_device_error(ctx);
@@ -466,6 +749,7 @@ int pic_set_fields(pic_ctx *ctx, const double *f)
     }
     launch_fill_ghosts(g, ctx->EB, 6, ctx->st);
     ctx->launches += 1;
+    ctx->ghosts_stale = ctx->slabs;   // z ghost planes come from the neighbours
     PIC_CUDA(ctx, cudaGetLastError());
     PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return PIC_OK;
@@ -490,32 +774,72 @@ int pic_get_fields(pic_ctx *ctx, double *f)
     return PIC_OK;
 }
 
+static int device_slots(pic_ctx *ctx, int species, int64_t *n)
+{
+    PIC_CUDA(ctx, cudaMemcpyAsync(n, ctx->dev_n + species, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->st));
+    PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return PIC_OK;
+}
+
 int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout, double *x, double *y, double *z,
                       double *ux, double *uy, double *uz, uint64_t *id)
 {
     if (!ctx || !n_inout) return PIC_EINVAL;
     if (species < 0 || species >= ctx->cfg.n_species) return fail(ctx, PIC_EINVAL, "bad species");
-    const int64_t n = ctx->count[species];
-    const int64_t capacity = *n_inout;
-    *n_inout = n;
-    if (capacity < n) return fail(ctx, PIC_ECAPACITY, "output arrays too small");
+    int64_t slots = 0;
+    int rc = device_slots(ctx, species, &slots);
+    if (rc != PIC_OK) return rc;
     const ParticlesDev &A = ctx->A[species];
     const double *src[6] = {A.x, A.y, A.z, A.ux, A.uy, A.uz};
     double *dst[6] = {x, y, z, ux, uy, uz};
-    for (int c = 0; c < 6 && n > 0; ++c)
-        if (dst[c])
-            PIC_CUDA(ctx, cudaMemcpyAsync(dst[c], src[c], sizeof(double) * (size_t)n,
+    const int64_t capacity = *n_inout;
+    if (!ctx->slabs) {   // every slot is live
+        *n_inout = slots;
+        if (capacity < slots) return fail(ctx, PIC_ECAPACITY, "output arrays too small");
+        for (int c = 0; c < 6 && slots > 0; ++c)
+            if (dst[c])
+                PIC_CUDA(ctx, cudaMemcpyAsync(dst[c], src[c], sizeof(double) * (size_t)slots,
+                                              cudaMemcpyDeviceToHost, ctx->st));
+        if (id && slots > 0)
+            PIC_CUDA(ctx, cudaMemcpyAsync(id, A.id, sizeof(uint64_t) * (size_t)slots, cudaMemcpyDeviceToHost, ctx->st));
+        PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        return PIC_OK;
+    }
+    // slabs: skip dead slots (x == -1) left by migration
+    std::vector<double> buf[6];
+    std::vector<uint64_t> ibuf((size_t)slots);
+    for (int c = 0; c < 6; ++c) {
+        buf[c].resize((size_t)slots);
+        if (slots > 0)
+            PIC_CUDA(ctx, cudaMemcpyAsync(buf[c].data(), src[c], sizeof(double) * (size_t)slots,
                                           cudaMemcpyDeviceToHost, ctx->st));
-    if (id && n > 0)
-        PIC_CUDA(ctx, cudaMemcpyAsync(id, A.id, sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    if (slots > 0)
+        PIC_CUDA(ctx, cudaMemcpyAsync(ibuf.data(), A.id, sizeof(uint64_t) * (size_t)slots, cudaMemcpyDeviceToHost, ctx->st));
     PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    int64_t live = 0;
+    for (int64_t p = 0; p < slots; ++p) live += buf[0][(size_t)p] >= 0.0;
+    *n_inout = live;
+    if (capacity < live) return fail(ctx, PIC_ECAPACITY, "output arrays too small");
+    int64_t k = 0;
+    for (int64_t p = 0; p < slots; ++p) {
+        if (buf[0][(size_t)p] < 0.0) continue;
+        for (int c = 0; c < 6; ++c)
+            if (dst[c]) dst[c][k] = buf[c][(size_t)p];
+        if (id) id[k] = ibuf[(size_t)p];
+        ++k;
+    }
     return PIC_OK;
 }
 
 int pic_get_count(pic_ctx *ctx, int species, int64_t *n)
 {
     if (!ctx || !n || species < 0 || species >= ctx->cfg.n_species) return PIC_EINVAL;
-    *n = ctx->count[species];
+    if (!ctx->slabs) return device_slots(ctx, species, n);
+    int64_t cap = 0;
+    int rc = pic_get_particles(ctx, species, &cap, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (rc != PIC_OK && rc != PIC_ECAPACITY) return rc;
+    *n = cap;
     return PIC_OK;
 }
 
@@ -529,9 +853,16 @@ int pic_get_step_index(pic_ctx *ctx, int64_t *n)
 int pic_step(pic_ctx *ctx, int64_t nsteps)
 {
     if (!ctx || nsteps < 0) return PIC_EINVAL;
+    if (ctx->local_group) return fail(ctx, PIC_ESTATE, "PIC_FLAG_LOCAL_GROUP contexts step via pic_step_group");
     const int64_t K = ctx->cfg.sort_every;
     const bool profile = (ctx->cfg.flags & PIC_FLAG_PROFILE) != 0;
     const bool use_graph = !profile && !(ctx->cfg.flags & PIC_FLAG_NO_GRAPH) && ctx->st != nullptr;
+    if (ctx->ghosts_stale && nsteps > 0) {
+        std::vector<Msg> m = msgs_fields(ctx, 0, 6);
+        int rc = exchange_nccl(ctx, m);
+        if (rc != PIC_OK) return rc;
+        ctx->ghosts_stale = false;
+    }
     for (int64_t s = 0; s < nsteps; ++s) {
         const bool sort_now = K > 0 && (ctx->step_index % K) == 0;
         const int jc = ctx->jcur;
@@ -547,7 +878,9 @@ int pic_step(pic_ctx *ctx, int64_t nsteps)
             PIC_CUDA(ctx, cudaGraphLaunch(ctx->graph[sort_now][jc], ctx->st));
             ctx->launches += ctx->graph_launches[sort_now][jc];
         } else {
-            ctx->launches += enqueue_step(ctx, sort_now, jc, profile);
+            const int n = enqueue_step(ctx, sort_now, jc, profile);
+            if (n < 0) return PIC_ENCCL;
+            ctx->launches += n;
             PIC_CUDA(ctx, cudaGetLastError());
         }
         ctx->jlast = jc;
@@ -555,14 +888,53 @@ int pic_step(pic_ctx *ctx, int64_t nsteps)
         ctx->step_index++;
     }
     int rc = check_device_error(ctx);
-    if (profile) {
-        for (auto &m : ctx->ev_marks) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, m.second.first, m.second.second);
-            ctx->stage_ms[m.first] += ms;
+    if (profile) collect_profile(ctx);
+    return rc;
+}
+
+int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps)
+{
+    if (!ctxs || n < 1 || nsteps < 0) return PIC_EINVAL;
+    for (int r = 0; r < n; ++r) {
+        if (!ctxs[r] || !ctxs[r]->local_group || ctxs[r]->cfg.nranks != n || ctxs[r]->cfg.rank != r)
+            return fail(ctxs[r], PIC_EINVAL, "pic_step_group needs PIC_FLAG_LOCAL_GROUP ranks 0..n-1");
+    }
+    auto all = [&](auto f) {
+        std::vector<std::vector<Msg>> m(n);
+        for (int r = 0; r < n; ++r) m[r] = f(ctxs[r]);
+        return m;
+    };
+    if (ctxs[0]->ghosts_stale && nsteps > 0) {
+        int rc = exchange_local(ctxs, n, all([](pic_ctx *c) { return msgs_fields(c, 0, 6); }));
+        if (rc != PIC_OK) return rc;
+        for (int r = 0; r < n; ++r) ctxs[r]->ghosts_stale = false;
+    }
+    for (int64_t s = 0; s < nsteps; ++s) {
+        const int64_t K = ctxs[0]->cfg.sort_every;
+        const bool sort_now = K > 0 && (ctxs[0]->step_index % K) == 0;
+        const int jc = ctxs[0]->jcur;
+        for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_push(ctxs[r], sort_now, jc, false);
+        int rc = exchange_local(ctxs, n, all([jc](pic_ctx *c) { return msgs_current(c, jc); }));
+        if (rc != PIC_OK) return rc;
+        for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_fields_e(ctxs[r], jc, false);
+        rc = exchange_local(ctxs, n, all([](pic_ctx *c) { return msgs_fields(c, 0, 3); }));
+        if (rc != PIC_OK) return rc;
+        for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_fields_b(ctxs[r], false);
+        rc = exchange_local(ctxs, n, all([](pic_ctx *c) { return msgs_fields(c, 3, 6); }));
+        if (rc != PIC_OK) return rc;
+        for (int r = 0; r < n; ++r) {
+            pic_ctx *c = ctxs[r];
+            for (int sp = 0; sp < c->cfg.n_species; ++sp) c->has_particles[sp] = true;
+            c->jlast = jc;
+            c->jcur = 1 - jc;
+            c->step_index++;
         }
-        ctx->ev_marks.clear();
-        ctx->ev_used = 0;
+    }
+    int rc = PIC_OK;
+    for (int r = 0; r < n; ++r) {
+        PIC_CUDA(ctxs[r], cudaGetLastError());
+        const int e = check_device_error(ctxs[r]);
+        if (e != PIC_OK && rc == PIC_OK) rc = e;
     }
     return rc;
 }
@@ -600,6 +972,10 @@ void pic_destroy(pic_ctx *ctx)
     if (!ctx) return;
     destroy_graphs(ctx);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->comm) {
+        NcclApi *api = nccl_api();
+        if (api) api->commDestroy(ctx->comm);
+    }
     delete ctx;
 }
 

@@ -19,6 +19,8 @@
 //      sc_off[s] = start[s * S^3].
 // The key uses floor(x / dx) with an IEEE division, the same decision the
 // oracle takes (DESIGN.md sec. 3 R15), so permutations are bit-identical.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace pic {
@@ -36,24 +38,32 @@ __device__ __forceinline__ int cell_of(double x, double d, int n_local, int offs
     return c >= n_local ? n_local - 1 : c;
 }
 
+constexpr uint32_t kDeadKey = 0xffffffffu;
+
 __global__ void __launch_bounds__(256)
-k_sort_key(GridDev g, ParticlesDev src, int64_t n, uint32_t *__restrict__ key,
+k_sort_key(GridDev g, ParticlesDev src, const int64_t *__restrict__ dev_n, uint32_t *__restrict__ key,
            uint32_t *__restrict__ slot, uint32_t *__restrict__ count, unsigned *err)
 {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const double x = src.x[p], y = src.y[p], z = src.z[p];
-    if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= 0.0 && z < g.Lz))
-        atomicOr(err, isfinite(x) && isfinite(y) && isfinite(z) ? kErrRange : kErrNonFinite);
-    const int cx = cell_of(x, g.dx, g.nx, 0);
-    const int cy = cell_of(y, g.dy, g.ny, 0);
-    const int cz = cell_of(z, g.dz, g.nz, g.k0);
-    const int S = g.S;
-    const uint32_t sc = (uint32_t)((cx / S) + g.nsx * ((cy / S) + g.nsy * (cz / S)));
-    const uint32_t loc = (uint32_t)((cx % S) + S * ((cy % S) + S * (cz % S)));
-    const uint32_t k = sc * (uint32_t)(S * S * S) + loc;
-    key[p] = k;
-    slot[p] = atomicAdd(count + k, 1u);
+    const int64_t n = *dev_n;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const double x = src.x[p], y = src.y[p], z = src.z[p];
+        if (x == kDeadX) {   // slot left by a particle that migrated: dropped here
+            key[p] = kDeadKey;
+            continue;
+        }
+        if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= g.zlo && z < g.zhi))
+            atomicOr(err, isfinite(x) && isfinite(y) && isfinite(z) ? kErrRange : kErrNonFinite);
+        const int cx = cell_of(x, g.dx, g.nx, 0);
+        const int cy = cell_of(y, g.dy, g.ny, 0);
+        const int cz = cell_of(z, g.dz, g.nz, g.k0);
+        const int S = g.S;
+        const uint32_t sc = (uint32_t)((cx / S) + g.nsx * ((cy / S) + g.nsy * (cz / S)));
+        const uint32_t loc = (uint32_t)((cx % S) + S * ((cy % S) + S * (cz % S)));
+        const uint32_t k = sc * (uint32_t)(S * S * S) + loc;
+        key[p] = k;
+        slot[p] = atomicAdd(count + k, 1u);
+    }
 }
 
 // ---- exclusive scan of uint32 (counts fit: n < 2^31) ----
@@ -142,11 +152,15 @@ k_scan_add(const uint32_t *__restrict__ in, int64_t n, const uint32_t *__restric
 
 __global__ void __launch_bounds__(256)
 k_scatter(const uint32_t *__restrict__ key, const uint32_t *__restrict__ slot,
-          const uint32_t *__restrict__ start, int64_t n, uint32_t *__restrict__ perm_tmp)
+          const uint32_t *__restrict__ start, const int64_t *__restrict__ dev_n,
+          uint32_t *__restrict__ perm_tmp)
 {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    perm_tmp[start[key[p]] + slot[p]] = (uint32_t)p;
+    const int64_t n = *dev_n;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = key[p];
+        if (k != kDeadKey) perm_tmp[start[k] + slot[p]] = (uint32_t)p;
+    }
 }
 
 // one warp per bucket: perm[start + rank(v)] = v with rank = #{u < v}
@@ -215,59 +229,58 @@ k_interleave(const uint32_t *__restrict__ start, int cps, const uint32_t *__rest
 }
 
 __global__ void __launch_bounds__(256)
-k_gather(ParticlesDev src, ParticlesDev dst, const uint32_t *__restrict__ perm, int64_t n)
+k_gather(ParticlesDev src, ParticlesDev dst, const uint32_t *__restrict__ perm,
+         const uint32_t *__restrict__ live)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t p = perm[i];
-    dst.x[i] = src.x[p];
-    dst.y[i] = src.y[p];
-    dst.z[i] = src.z[p];
-    dst.ux[i] = src.ux[p];
-    dst.uy[i] = src.uy[p];
-    dst.uz[i] = src.uz[p];
-    dst.id[i] = src.id[p];
+    const int64_t n = *live;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = perm[i];
+        dst.x[i] = src.x[p];
+        dst.y[i] = src.y[p];
+        dst.z[i] = src.z[p];
+        dst.ux[i] = src.ux[p];
+        dst.uy[i] = src.uy[p];
+        dst.uz[i] = src.uz[p];
+        dst.id[i] = src.id[p];
+    }
 }
 
+// supercell offsets; the particle count becomes the number of live particles
 __global__ void k_sc_offsets(const uint32_t *__restrict__ start, int64_t n_sc, int cells_per_sc,
-                             int64_t *__restrict__ sc_off)
+                             int64_t *__restrict__ sc_off, int64_t *__restrict__ dev_n)
 {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s > n_sc) return;
     sc_off[s] = (int64_t)start[s * cells_per_sc];
+    if (s == n_sc) *dev_n = (int64_t)start[s * cells_per_sc];
 }
 
-void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst, int64_t n,
-                    const SortScratch &s, int64_t *sc_off, unsigned *err, cudaStream_t st,
-                    int *launches)
+void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst,
+                    int64_t *dev_n, int64_t cap, const SortScratch &s, int64_t *sc_off,
+                    unsigned *err, cudaStream_t st, int *launches)
 {
     const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
     const int64_t n_sc = (int64_t)g.nsx * g.nsy * g.nsz;
-    const int64_t nscan = ncells + 1;   // count[ncells] stays 0 -> start[ncells] = n
+    const int64_t nscan = ncells + 1;   // count[ncells] stays 0 -> start[ncells] = live count
     int L = 0;
     cudaMemsetAsync(s.count, 0, sizeof(uint32_t) * (size_t)nscan, st);
     const int bs = 256;
-    if (n > 0) {
-        k_sort_key<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(g, src, n, s.key, s.slot, s.count, err);
-        ++L;
-    }
+    const unsigned pblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((cap + bs - 1) / bs, 148 * 64));
+    k_sort_key<<<pblocks, bs, 0, st>>>(g, src, dev_n, s.key, s.slot, s.count, err);
     const int64_t nb = (int64_t)scan_block_count(nscan);
     k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(s.count, nscan, s.block_sums);
     k_scan_blocks<<<1, kScanThreads, 0, st>>>(s.block_sums, nb);
     k_scan_add<<<(unsigned)nb, kScanThreads, 0, st>>>(s.count, nscan, s.block_sums, s.start);
-    L += 3;
-    if (n > 0) {
-        k_scatter<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(s.key, s.slot, s.start, n, s.perm_tmp);
-        const int64_t threads = ncells * 32;
-        k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);
-        const int cps = g.S * g.S * g.S;
-        k_interleave<<<(unsigned)n_sc, bs, sizeof(uint32_t) * (2 * cps + 1), st>>>(s.start, cps, s.perm,
-                                                                               s.perm_tmp);
-        k_gather<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(src, dst, s.perm_tmp, n);
-        L += 4;
-    }
-    k_sc_offsets<<<(unsigned)((n_sc + 1 + bs - 1) / bs), bs, 0, st>>>(s.start, n_sc, g.S * g.S * g.S, sc_off);
-    ++L;
+    k_scatter<<<pblocks, bs, 0, st>>>(s.key, s.slot, s.start, dev_n, s.perm_tmp);
+    const int64_t threads = ncells * 32;
+    k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);
+    const int cps = g.S * g.S * g.S;
+    k_interleave<<<(unsigned)n_sc, bs, sizeof(uint32_t) * (2 * cps + 1), st>>>(s.start, cps, s.perm,
+                                                                           s.perm_tmp);
+    k_gather<<<pblocks, bs, 0, st>>>(src, dst, s.perm_tmp, s.start + ncells);
+    k_sc_offsets<<<(unsigned)((n_sc + 1 + bs - 1) / bs), bs, 0, st>>>(s.start, n_sc, cps, sc_off, dev_n);
+    L += 10;
     if (launches) *launches += L;
 }
 

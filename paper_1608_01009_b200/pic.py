@@ -25,12 +25,13 @@ ERRORS = {
 FLAG_NO_GRAPH = 1
 FLAG_PROFILE = 2
 FLAG_NAIVE = 4
+FLAG_LOCAL_GROUP = 8
 
 EXPORTS = [
     "pic_workspace_size", "pic_init", "pic_set_particles", "pic_set_fields", "pic_step",
     "pic_get_fields", "pic_get_particles", "pic_get_count", "pic_get_step_index",
     "pic_get_stage_times", "pic_get_launch_count", "pic_strerror", "pic_last_error",
-    "pic_destroy",
+    "pic_destroy", "pic_nccl_unique_id", "pic_step_group",
 ]
 
 
@@ -48,6 +49,7 @@ class PicConfig(C.Structure):
         ("sort_every", C.c_int64),
         ("rank", C.c_int64), ("nranks", C.c_int64),
         ("flags", C.c_int64),
+        ("migrate_capacity", C.c_int64),
         ("nccl_id", C.c_uint8 * 128),
         ("stream", C.c_void_p),
     ]
@@ -88,6 +90,8 @@ def lib():
         L.pic_last_error.restype = C.c_char_p
         L.pic_destroy.argtypes = [C.c_void_p]
         L.pic_destroy.restype = None
+        L.pic_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.pic_step_group.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int64]
         for name in EXPORTS:
             if name not in ("pic_strerror", "pic_last_error", "pic_destroy"):
                 getattr(L, name).restype = C.c_int
@@ -100,7 +104,8 @@ def _dptr(a):
 
 
 def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity=None,
-                supercell=4, sort_every=20, rank=0, nranks=1, flags=0, nccl_id=None):
+                supercell=4, sort_every=20, rank=0, nranks=1, flags=0, nccl_id=None,
+                migrate_capacity=0):
     """species: list of (q, m, w)."""
     cfg = PicConfig()
     cfg.nx, cfg.ny, cfg.nz = nx, ny, nz
@@ -112,6 +117,7 @@ def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity
         cfg.capacity[i] = 0 if capacity is None else int(capacity[i])
     cfg.supercell, cfg.sort_every = supercell, sort_every
     cfg.rank, cfg.nranks, cfg.flags = rank, nranks, flags
+    cfg.migrate_capacity = migrate_capacity
     if nccl_id is not None:
         C.memmove(cfg.nccl_id, bytes(nccl_id), 128)
     return cfg
@@ -221,16 +227,61 @@ class Simulation:
             pass
 
 
-def simulation_from_workload(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
-                             sort_every=None, nccl_id=None, counts=None):
-    """Build a Simulation for a synth.Workload (species q, m, w, dt from the workload)."""
+def workload_config(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
+                    sort_every=None, nccl_id=None, counts=None, migrate_capacity=0):
+    """pic_config for a synth.Workload (species q, m, w, dt from the workload).
+
+    With nranks > 1 this rank holds the z slab [rank nz/nranks, (rank+1) nz/nranks)
+    and the default capacity leaves 10% headroom for migration."""
     species = [(s.q, s.m, s.w) for s in wl.species]
     nz_local = wl.nz // nranks
     if counts is None:
         counts = [s.ppc * wl.nx * wl.ny * nz_local for s in wl.species]
+        if nranks > 1:
+            capacity_factor = max(capacity_factor, 1.1)
     cap = [max(1, int(np.ceil(c * capacity_factor))) for c in counts]
-    cfg = make_config(wl.nx, wl.ny, wl.nz, species, wl.dt, wl.dx, wl.dy, wl.dz, wl.c, cap,
-                      supercell or wl.supercell,
-                      wl.sort_every if sort_every is None else sort_every,
-                      rank, nranks, flags, nccl_id)
-    return Simulation(cfg)
+    return make_config(wl.nx, wl.ny, wl.nz, species, wl.dt, wl.dx, wl.dy, wl.dz, wl.c, cap,
+                       supercell or wl.supercell,
+                       wl.sort_every if sort_every is None else sort_every,
+                       rank, nranks, flags, nccl_id, migrate_capacity)
+
+
+def simulation_from_workload(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
+                             sort_every=None, nccl_id=None, counts=None, migrate_capacity=0,
+                             stream=None):
+    """Build a Simulation for a synth.Workload."""
+    cfg = workload_config(wl, capacity_factor, flags, rank, nranks, supercell, sort_every,
+                          nccl_id, counts, migrate_capacity)
+    return Simulation(cfg, stream=stream)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from libpic's NCCL loader (rank 0 of a slab run)."""
+    buf = (C.c_uint8 * 128)()
+    rc = lib().pic_nccl_unique_id(buf)
+    if rc != PIC_OK:
+        raise PicError(rc, "pic_nccl_unique_id")
+    return bytes(buf)
+
+
+def broadcast_nccl_id(id_bytes, group=None) -> bytes:
+    """Distributes rank 0's NCCL id over an initialised torch.distributed group
+    (gloo or nccl).  Plumbing only: the exchange itself runs inside libpic."""
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if dist.get_rank(group) == 0:
+        t.copy_(torch.frombuffer(bytearray(id_bytes), dtype=torch.uint8))
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().tolist())
+
+
+def step_group(sims, nsteps=1):
+    """Advance PIC_FLAG_LOCAL_GROUP slab Simulations (ranks 0..n-1 on one GPU) together."""
+    arr = (C.c_void_p * len(sims))(*[s.ctx.value for s in sims])
+    rc = lib().pic_step_group(arr, len(sims), int(nsteps))
+    if rc != PIC_OK:
+        msgs = "; ".join(lib().pic_last_error(s.ctx).decode() for s in sims)
+        raise PicError(rc, msgs)

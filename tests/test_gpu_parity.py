@@ -318,3 +318,69 @@ def test_c2_full_size_sampled_and_properties(pic, oracle_mod):
     tot = sp.q * sp.w * v.sum(axis=1)
     got = F1[6:].sum(axis=(1, 2, 3))
     np.testing.assert_allclose(got, tot, rtol=1e-9, atol=1e-12 * np.abs(tot).max())
+
+
+# ---------------------------------------------------------------- z slabs (a8, sec. 8e)
+
+def _slab_group(pic, wl, nranks, stream):
+    sims = []
+    for r in range(nranks):
+        cfg = pic.workload_config(wl, rank=r, nranks=nranks, flags=pic.FLAG_LOCAL_GROUP,
+                                  migrate_capacity=4096)
+        sims.append(pic.Simulation(cfg, stream=stream))
+    return sims
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_slab_decomposition_matches_single_domain_oracle(pic, oracle_mod, nranks):
+    """The z-slab path (J ghost planes summed by the owner, E/B ghost planes,
+    particle migration, unsorted arrivals tail) run as an in-process group of
+    slab contexts on one GPU, against the single-domain oracle (P16)."""
+    import torch
+    from synth import gen_particles, get_config
+    from synth.configs import electron
+    wl = get_config("C1").with_(species=(electron(6, 0.2),), nz=16, sort_every=5)
+    parts = gen_particles(wl)
+    rng = np.random.default_rng(21)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.02
+    orc = _oracle_for(oracle_mod, wl, parts)
+    orc.F[:6] = F6
+    stream = torch.cuda.Stream()
+    sims = _slab_group(pic, wl, nranks, stream)
+    nzl = wl.nz // nranks
+    for r, sim in enumerate(sims):
+        sim.set_particles(0, *parts[0])
+        sim.set_fields(F6[:, r * nzl:(r + 1) * nzl].copy())
+    L = _L(wl)
+    migrated = 0
+    for step in range(15):
+        orc.step(1)
+        pic.step_group(sims, 1)
+        G = np.concatenate([s.get_fields() for s in sims], axis=1)
+        Ps, Is = zip(*[s.get_particles(0) for s in sims])
+        gP, gi = np.concatenate(Ps, axis=1), np.concatenate(Is)
+        for r, (P_r, _) in enumerate(zip(Ps, Is)):   # every particle lives in its rank's slab
+            assert (P_r[2] >= r * nzl * wl.dz).all() and (P_r[2] < (r + 1) * nzl * wl.dz).all()
+        pe, ue = compare_state(gP, gi, orc.P[0], orc.ids[0], L)
+        errs = field_errs(G, orc.F) + [pe, ue]
+        assert max(errs) <= 1e-11, (step, errs)
+        migrated += sum(P_r.shape[1] for P_r in Ps)
+    assert migrated > 0
+
+
+def test_slab_migration_capacity_error(pic):
+    import torch
+    from synth import gen_particles, get_config
+    from synth.configs import electron
+    wl = get_config("C1").with_(species=(electron(8, 0.3),), nz=16, sort_every=5)
+    parts = gen_particles(wl)
+    stream = torch.cuda.Stream()
+    sims = []
+    for r in range(2):
+        cfg = pic.workload_config(wl, rank=r, nranks=2, flags=pic.FLAG_LOCAL_GROUP, migrate_capacity=4)
+        sims.append(pic.Simulation(cfg, stream=stream))
+    for sim in sims:
+        sim.set_particles(0, *parts[0])
+    with pytest.raises(pic.PicError) as e:
+        pic.step_group(sims, 3)
+    assert e.value.code == -3
