@@ -36,7 +36,8 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 void configure_tile_kernels();
 void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
                       const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                      const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st);
+                      const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
+                      cudaStream_t st);
 
 // ---- sort.cu : stable counting sort by (supercell, local cell) ----
 struct SortScratch {

@@ -128,9 +128,13 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
         const long long bits = __double_as_longlong(fma(v, scale, kMagic));
         const unsigned lo = (unsigned)bits;
         const unsigned hi = ((unsigned)(bits >> 32) & 0xfffffu) - (1u << 19);
+#ifdef PIC_EXP_NOATOMICS   // timing experiment only: drop the tile atomics
+        if (lo == 0x12345u && hi == 0x777u) b[off] = 1u;
+#else
         atomicAdd(b + off, lo & 0xffffu);
         atomicAdd(b + 3 * NJ + off, lo >> 16);
         atomicAdd(b + 6 * NJ + off, hi);
+#endif
     };
     add(0, fx * fma(ny, nz, cxx));
     add(PX, fx * fma(my, nz, -cxx));
@@ -171,7 +175,7 @@ template <int S, int H>
 __global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
 k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
             double *__restrict__ J, ParticlesDev in, ParticlesDev out,
-            const int64_t *__restrict__ sc_off, SpeciesDev sp, int copy_id, unsigned *err)
+            const int64_t *__restrict__ sc_off, SpeciesDev sp, int copy_id, int split, unsigned *err)
 {
     using T = TileGeom<S, H>;
     constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = kTileThreads;
@@ -185,9 +189,13 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     unsigned *qcount = qcell + kQueue;
     uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);
     const int tid = threadIdx.x, lane = tid & 31;
-    const int sc = blockIdx.x;
-    const int p0 = (int)sc_off[sc], p1 = (int)sc_off[sc + 1];
-    if (p0 == p1) return;   // empty supercell (uniform per CTA)
+    // `split` CTAs share a supercell, each taking a contiguous part of its
+    // particles (short grids fill the last wave; each CTA has its own tiles)
+    const int sc = blockIdx.x / split, part = blockIdx.x % split;
+    const int P0 = (int)sc_off[sc], P1 = (int)sc_off[sc + 1];
+    const int p0 = P0 + (int)(((int64_t)(P1 - P0) * part) / split);
+    const int p1 = P0 + (int)(((int64_t)(P1 - P0) * (part + 1)) / split);
+    if (p0 == p1) return;   // empty (uniform per CTA)
 
     const int scx = sc % g.nsx, scy = (sc / g.nsx) % g.nsy, scz = sc / (g.nsx * g.nsy);
     // local-grid coordinates of the tile origin (same for the E/B and J tiles)
@@ -253,13 +261,25 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                             (unsigned)(ty - 1) < (unsigned)(S + 2 * H) &&
                             (unsigned)(tz - 1) < (unsigned)(S + 2 * H);
         if (inside) {
+#ifdef PIC_EXP_NOGATHER   // timing experiment only: same node for every lane
+            const int hx = 2, hy = 2, hz = 2;
+#define tx 2
+#define ty 2
+#define tz 2
+#else
             const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
+#endif
             const double ex = trilinear(eb + 0 * NE, hx + EPX * ty + EPY * tz, EPX, EPY, wx.fh, wy.f0, wz.f0);
             const double ey = trilinear(eb + 1 * NE, tx + EPX * hy + EPY * tz, EPX, EPY, wx.f0, wy.fh, wz.f0);
             const double ez = trilinear(eb + 2 * NE, tx + EPX * ty + EPY * hz, EPX, EPY, wx.f0, wy.f0, wz.fh);
             const double bx = trilinear(eb + 3 * NE, tx + EPX * hy + EPY * hz, EPX, EPY, wx.f0, wy.fh, wz.fh);
             const double by = trilinear(eb + 4 * NE, hx + EPX * ty + EPY * hz, EPX, EPY, wx.fh, wy.f0, wz.fh);
             const double bz = trilinear(eb + 5 * NE, hx + EPX * hy + EPY * tz, EPX, EPY, wx.fh, wy.fh, wz.f0);
+#ifdef PIC_EXP_NOGATHER
+#undef tx
+#undef ty
+#undef tz
+#endif
             boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
             const double ig = rsqrt_ge1(1.0 + (ux * ux + uy * uy + uz * uz));
             const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
@@ -348,12 +368,18 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 template <int S, int H>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
                         const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                        const SpeciesDev &sp, bool copy_id, unsigned *err, cudaStream_t st)
+                        const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
+                        cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
-    const int nsc = g.nsx * g.nsy * g.nsz;   // one CTA per supercell (empty ones exit at once)
-    k_push_tile<S, H><<<nsc, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
-                                                       copy_id ? 1 : 0, err);
+    const int nsc = g.nsx * g.nsy * g.nsz;
+    // one CTA per supercell (empty ones exit at once); only very dense
+    // supercells (> 8192 particles expected) are split over several CTAs --
+    // splitting C2's 3200-particle supercells was measured slower (extra tile
+    // loads and flushes outweigh the shorter last wave)
+    const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + 8191) / 8192));
+    k_push_tile<S, H><<<nsc * split, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
+                                                               copy_id ? 1 : 0, split, err);
 }
 
 bool tile_supported(int S) { return S == 2 || S == 4; }
@@ -377,13 +403,13 @@ void configure_tile_kernels()
 
 void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
                       const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                      const SpeciesDev &sp, bool copy_id, unsigned *err, int num_sms, cudaStream_t st)
+                      const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
+                      cudaStream_t st)
 {
-    (void)num_sms;
     if (g.S == 4)
-        launch_tile<4, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, st);
+        launch_tile<4, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
     else if (g.S == 2)
-        launch_tile<2, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, st);
+        launch_tile<2, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
 }
 
 }  // namespace pic

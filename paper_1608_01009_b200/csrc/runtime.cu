@@ -434,7 +434,7 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
         const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
         if (ctx->use_tile)
             launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s], sp,
-                             sort_now, ctx->err, ctx->num_sms, ctx->st);
+                             sort_now, ctx->err, L.cap[s] / std::max<int64_t>(1, L.n_sc), ctx->st);
         else
             launch_push_tail(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], nullptr, ctx->dev_n + s, L.cap[s], sp,
                              sort_now, ctx->err, ctx->st);

@@ -384,3 +384,49 @@ def test_slab_migration_capacity_error(pic):
     with pytest.raises(pic.PicError) as e:
         pic.step_group(sims, 3)
     assert e.value.code == -3
+
+
+def test_supercell_two_tile_kernel(pic, oracle_mod):
+    """S = 2 instantiation of the fused kernel (6^3 E/B tile) against the oracle."""
+    from synth import get_config
+    wl = get_config("T_two_species").with_(supercell=2, sort_every=3)
+    rng = np.random.default_rng(22)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.05
+    _run_parity(pic, oracle_mod, wl, 8, teacher_forced=False, fields=F6, tol=1e-11)
+
+
+def test_dense_supercell_global_path(pic, oracle_mod):
+    """A supercell holding more particles than the fixed-point tile counters
+    allow (> 16383) is pushed through the global path; results unchanged."""
+    from synth import Workload
+    from synth.configs import electron
+    wl = Workload("dense", 8, 8, 8, (electron(300, 0.05),), steps=2, sort_every=2, supercell=4)
+    _run_parity(pic, oracle_mod, wl, 2, teacher_forced=True, tol=1e-12)
+
+
+def test_particles_on_faces_and_corners(pic, oracle_mod):
+    """Start points exactly on cell faces / edges / corners and moves that end
+    on faces (zero-length pieces of the VB split)."""
+    from synth import get_config
+    wl = get_config("T_small").with_(sort_every=1)
+    from synth import gen_particles
+    P, ids = gen_particles(wl)[0]
+    P = P.copy()
+    P[0, ::3] = np.floor(P[0, ::3])                  # x on a face
+    P[:2, 1::7] = np.floor(P[:2, 1::7])              # x, y on an edge
+    P[:3, 2::11] = np.floor(P[:3, 2::11])            # corner
+    P[3:, 5::13] = 0.0                               # at rest
+    orc = _oracle_for(oracle_mod, wl, [(P, ids)])
+    sim = _sim(pic, wl)
+    sim.set_particles(0, P, ids)
+    rng = np.random.default_rng(23)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.03
+    orc.F[:6] = F6
+    sim.set_fields(F6)
+    for _ in range(3):
+        orc.step(1)
+        sim.step(1)
+        G = sim.get_fields()
+        gP, gi = sim.get_particles(0)
+        pe, ue = compare_state(gP, gi, orc.P[0], orc.ids[0], _L(wl))
+        assert max(field_errs(G, orc.F) + [pe, ue]) <= 1e-12
