@@ -158,13 +158,16 @@ __device__ __forceinline__ bool vb_first_piece(double ax, double ay, double az, 
     ox = oy = oz = 0;
     if (crossing) {
         const double px = bx < 0.0 ? 0.0 : 1.0, py = by < 0.0 ? 0.0 : 1.0, pz = bz < 0.0 ? 0.0 : 1.0;
-        const double tx = cxq ? (px - ax) / (bx - ax) : 2.0;
-        const double ty = cyq ? (py - ay) / (by - ay) : 2.0;
-        const double tz = czq ? (pz - az) / (bz - az) : 2.0;
-        int axis = 0;
-        double t = tx;
-        if (ty < t) { t = ty; axis = 1; }
-        if (tz < t) { t = tz; axis = 2; }
+        // first crossing = smallest tau_d = |p_d - a_d| / |b_d - a_d|, compared by
+        // cross-multiplication (one division for the winner); ties keep the lower axis
+        const double nxd = fabs(px - ax), nyd = fabs(py - ay), nzd = fabs(pz - az);
+        const double dxd = fabs(bx - ax), dyd = fabs(by - ay), dzd = fabs(bz - az);
+        int axis = cxq ? 0 : (cyq ? 1 : 2);
+        double num = axis == 0 ? nxd : (axis == 1 ? nyd : nzd);
+        double den = axis == 0 ? dxd : (axis == 1 ? dyd : dzd);
+        if (cyq && axis < 1 && nyd * den < num * dyd) { axis = 1; num = nyd; den = dyd; }
+        if (czq && axis < 2 && nzd * den < num * dzd) { axis = 2; num = nzd; den = dzd; }
+        const double t = num / den;
         ex = fma(t, bx - ax, ax);
         ey = fma(t, by - ay, ay);
         ez = fma(t, bz - az, az);

@@ -30,6 +30,7 @@ namespace pic {
 
 constexpr int kTileThreads = 256;
 constexpr int kQueue = 160;     // per-supercell queue of path remainders (crossing particles)
+constexpr int kFQueue = 256;    // per-supercell queue of particles outside the tile (global path)
 constexpr int kCtasPerSm = 2;
 
 // Shared-memory tile geometry.  Row/plane pitches are padded so that the 32
@@ -56,7 +57,8 @@ struct TileGeom {
     static constexpr size_t off_q = off_part + 12 * kTileThreads * sizeof(double);   // [6][kQueue] fp64
     static constexpr size_t off_jt = off_q + 6 * kQueue * sizeof(double);      // [9][NJ] u32
     static constexpr size_t off_qcell = off_jt + 9 * NJ * sizeof(unsigned);    // [kQueue] u32
-    static constexpr size_t off_misc = (off_qcell + (kQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
+    static constexpr size_t off_fq = off_qcell + (kQueue + 1) * sizeof(unsigned);   // [kFQueue + 1] u32
+    static constexpr size_t off_misc = (off_fq + (kFQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
     static constexpr size_t smem_bytes = off_misc + sizeof(uint64_t);          // 1 mbarrier
 };
 
@@ -103,9 +105,10 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
     const double cyy = Dx * Dz * (1.0 / 12.0);
     const double czz = Dx * Dy * (1.0 / 12.0);
     const double nx = 1.0 - mx, ny = 1.0 - my, nz = 1.0 - mz;
-    // |value| <= |f| (1 + 1/12): weights are products of numbers in [0,1], |c| <= 1/12
-    const double fmaxv = fmax(fabs(fx), fmax(fabs(fy), fabs(fz)));
-    if (!(fmaxv * (13.0 / 12.0) * scale < 140737488355328.0)) {   // 2^47
+    // |value| <= |f| (1 + 1/12): weights are products of numbers in [0,1], |c| <= 1/12.
+    // f scaled by 2^F (exact): one fma per value then rounds f W 2^F + 1.5*2^52.
+    const double fxs = fx * scale, fys = fy * scale, fzs = fz * scale;
+    if (!(fmax(fabs(fxs), fmax(fabs(fys), fabs(fzs))) * (13.0 / 12.0) < 140737488355328.0)) {   // 2^47
         const int rem = jbase % PY, tx = rem % PX, ty = rem / PX, tz = jbase / PY;
         const int64_t X = g.X, XY = (int64_t)g.X * g.Y, cs = g.cs;
         double *b = J + gorigin + tx + X * ty + XY * tz;
@@ -124,10 +127,12 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
         return;
     }
     unsigned *b = jt + jbase;
-    auto add = [&](int off, double v) {
-        const long long bits = __double_as_longlong(fma(v, scale, kMagic));
+    // v = round(f W 2^F): the low word of y = v + 1.5*2^52 is v mod 2^32, the
+    // high word is 0x433 << 20 | (2^19 + (v >> 32))
+    auto add = [&](int off, double fs, double w) {
+        const long long bits = __double_as_longlong(fma(fs, w, kMagic));
         const unsigned lo = (unsigned)bits;
-        const unsigned hi = ((unsigned)(bits >> 32) & 0xfffffu) - (1u << 19);
+        const unsigned hi = (unsigned)(bits >> 32) - (0x43300000u + 0x80000u);
 #ifdef PIC_EXP_NOATOMICS   // timing experiment only: drop the tile atomics
         if (lo == 0x12345u && hi == 0x777u) b[off] = 1u;
 #else
@@ -136,18 +141,18 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
         atomicAdd(b + 6 * NJ + off, hi);
 #endif
     };
-    add(0, fx * fma(ny, nz, cxx));
-    add(PX, fx * fma(my, nz, -cxx));
-    add(PY, fx * fma(ny, mz, -cxx));
-    add(PX + PY, fx * fma(my, mz, cxx));
-    add(NJ, fy * fma(nx, nz, cyy));
-    add(NJ + 1, fy * fma(mx, nz, -cyy));
-    add(NJ + PY, fy * fma(nx, mz, -cyy));
-    add(NJ + 1 + PY, fy * fma(mx, mz, cyy));
-    add(2 * NJ, fz * fma(nx, ny, czz));
-    add(2 * NJ + 1, fz * fma(mx, ny, -czz));
-    add(2 * NJ + PX, fz * fma(nx, my, -czz));
-    add(2 * NJ + 1 + PX, fz * fma(mx, my, czz));
+    add(0, fxs, fma(ny, nz, cxx));
+    add(PX, fxs, fma(my, nz, -cxx));
+    add(PY, fxs, fma(ny, mz, -cxx));
+    add(PX + PY, fxs, fma(my, mz, cxx));
+    add(NJ, fys, fma(nx, nz, cyy));
+    add(NJ + 1, fys, fma(mx, nz, -cyy));
+    add(NJ + PY, fys, fma(nx, mz, -cyy));
+    add(NJ + 1 + PY, fys, fma(mx, mz, cyy));
+    add(2 * NJ, fzs, fma(nx, ny, czz));
+    add(2 * NJ + 1, fzs, fma(mx, ny, -czz));
+    add(2 * NJ + PX, fzs, fma(nx, my, -czz));
+    add(2 * NJ + 1 + PX, fzs, fma(mx, my, czz));
 }
 
 // Deposits the rest of a split path (<= 2 more face crossings) starting in
@@ -187,6 +192,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     unsigned *jt = (unsigned *)(smem_raw + T::off_jt);     // [3 chunks][3][TJ][JPY/..]
     unsigned *qcell = (unsigned *)(smem_raw + T::off_qcell);
     unsigned *qcount = qcell + kQueue;
+    unsigned *fq = (unsigned *)(smem_raw + T::off_fq);     // particles outside the tile
+    unsigned *fqcount = fq + kFQueue;
     uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);
     const int tid = threadIdx.x, lane = tid & 31;
     // `split` CTAs share a supercell, each taking a contiguous part of its
@@ -219,8 +226,15 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     };
     if (p0 + tid < p1) stage(p0 + tid, 0);
     cp_async_commit();
-    for (int t = tid; t < 9 * NJ; t += NT) jt[t] = 0u;
-    if (tid == 0) *qcount = 0u;
+    {   // zero the fixed-point J tile (16-byte stores)
+        uint4 *j4 = (uint4 *)jt;
+        for (int t = tid; t < (9 * NJ) / 4; t += NT) j4[t] = make_uint4(0u, 0u, 0u, 0u);
+        for (int t = (9 * NJ) / 4 * 4 + tid; t < 9 * NJ; t += NT) jt[t] = 0u;
+    }
+    if (tid == 0) {
+        *qcount = 0u;
+        *fqcount = 0u;
+    }
 
     const double kx = sp.qw / (g.dt * g.dy * g.dz);
     const double ky = sp.qw / (g.dt * g.dx * g.dz);
@@ -320,29 +334,46 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                                                                               : kErrNonFinite);
             }
         } else {
-            double xx = x, yy = y, zz = z;
-            push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
-            store_particle(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
-            u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+            // outside the tile (drifted > H cells since the sort): deferred to after
+            // the loop so the slow global path does not stall this warp's iteration
+            const unsigned slot = atomicAdd(fqcount, 1u);
+            if (slot < (unsigned)kFQueue) {
+                fq[slot] = (unsigned)p;
+            } else {
+                double xx = x, yy = y, zz = z;
+                push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+                store_particle(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
+                u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+            }
         }
     }
-    __syncthreads();   // all particles pushed, the remainder queue is complete
+    __syncthreads();   // all particles pushed, the queues are complete
     const int nq = min(*qcount, (unsigned)kQueue);
     for (int e = tid; e < nq; e += NT) {
         deposit_remainder<T>(jt, (int)qcell[e], J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
                              q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz, scale);
     }
+    const int nf = min(*fqcount, (unsigned)kFQueue);
+    for (int e = tid; e < nf; e += NT) {
+        const int p = (int)fq[e];
+        double xx = in.x[p], yy = in.y[p], zz = in.z[p], ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
+        push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+        store_particle(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
+        u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+    }
     __syncthreads();
-    // flush the fixed-point tile to the fp64 global J
+    // flush the fixed-point tile to the fp64 global J: one thread per (comp, z, y) row
     const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
-    for (int t = tid; t < 3 * NJ; t += NT) {
-        const int comp = t / NJ, r = t - comp * NJ;
-        const int a = r % JPY % JPX, b = (r % JPY) / JPX, c = r / JPY;
-        if (a >= TJ || b >= TJ) continue;   // padding
-        const long long fx = (long long)(int)jt[6 * NJ + t] * 4294967296LL +
-                             (long long)jt[3 * NJ + t] * 65536LL + (long long)jt[t];
-        if (fx != 0)
-            atomicAdd(J + comp * cs + gorigin + a + gsy * b + gsz * c, (double)fx * inv_scale);
+    for (int row = tid; row < 3 * TJ * TJ; row += NT) {
+        const int comp = row / (TJ * TJ), c = (row / TJ) % TJ, b = row % TJ;
+        const int base = comp * NJ + c * JPY + b * JPX;
+        double *Jrow = J + comp * cs + gorigin + gsy * b + gsz * c;
+#pragma unroll
+        for (int a = 0; a < TJ; ++a) {
+            const long long fx = (long long)(int)jt[6 * NJ + base + a] * 4294967296LL +
+                                 (long long)jt[3 * NJ + base + a] * 65536LL + (long long)jt[base + a];
+            if (fx != 0) atomicAdd(Jrow + a, (double)fx * inv_scale);
+        }
     }
     {
         const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc) >> 32));
