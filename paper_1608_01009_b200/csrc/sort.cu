@@ -31,9 +31,13 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 
 size_t scan_block_count(int64_t nitems) { return (size_t)((nitems + kScanTile - 1) / kScanTile); }
 
+// floor(x / d) -- the oracle's decision (an IEEE division); for a power-of-two
+// d the product with 1/d is the same exact quotient and much cheaper
 __device__ __forceinline__ int cell_of(double x, double d, int n_local, int offset)
 {
-    int c = (int)floor(x / d) - offset;
+    const double inv = 1.0 / d;
+    const bool pow2 = (inv * d == 1.0) && ((__double_as_longlong(d) & 0x000fffffffffffffLL) == 0);
+    int c = (int)floor(pow2 ? x * inv : x / d) - offset;
     c = c < 0 ? 0 : c;
     return c >= n_local ? n_local - 1 : c;
 }
@@ -210,6 +214,43 @@ k_interleave(const uint32_t *__restrict__ start, int cps, const uint32_t *__rest
     }
     __syncthreads();
     const uint32_t n = cum[cps];
+    // slot tables (cps <= 64): mask[r] = cells holding more than r particles,
+    // sbase[r] = number of particles in slots < r; then the slot-major position
+    // of (cell c, slot r) is sbase[r] + popc(mask[r] & cells below c)
+    constexpr int kMaxSlots = 2048;
+    __shared__ unsigned long long mask[kMaxSlots];
+    __shared__ uint32_t sbase[kMaxSlots + 1];
+    __shared__ uint32_t maxcnt;
+    if (threadIdx.x == 0) maxcnt = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < cps; c += blockDim.x) atomicMax(&maxcnt, cnt[c]);
+    __syncthreads();
+    const uint32_t R = maxcnt;
+    const bool tables = cps <= 64 && R <= (uint32_t)kMaxSlots;
+    if (tables) {
+        for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
+            unsigned long long m = 0ull;
+            for (int c = 0; c < cps; ++c) m |= (cnt[c] > r ? 1ull : 0ull) << c;
+            mask[r] = m;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {   // exclusive scan of popc(mask[r]) by one warp
+            uint32_t carry = 0;
+            for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+                const uint32_t r = r0 + threadIdx.x;
+                const uint32_t v = r < R ? (uint32_t)__popcll(mask[r]) : 0u;
+                uint32_t inc = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if ((int)threadIdx.x >= o) inc += t;
+                }
+                if (r < R) sbase[r] = carry + inc - v;
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        __syncthreads();
+    }
     for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) {
         // cell of q: last c with cum[c] <= q (binary search over cps+1 offsets)
         int lo = 0, hi = cps;
@@ -219,10 +260,15 @@ k_interleave(const uint32_t *__restrict__ start, int cps, const uint32_t *__rest
         }
         const int c = lo;
         const uint32_t r = q - cum[c];
-        uint32_t pos = 0;
-        for (int cc = 0; cc < cps; ++cc) {
-            const uint32_t m = cnt[cc];
-            pos += min(m, r) + ((cc < c && m > r) ? 1u : 0u);
+        uint32_t pos;
+        if (tables) {
+            pos = sbase[r] + (uint32_t)__popcll(mask[r] & ((1ull << c) - 1ull));
+        } else {
+            pos = 0;
+            for (int cc = 0; cc < cps; ++cc) {
+                const uint32_t m = cnt[cc];
+                pos += min(m, r) + ((cc < c && m > r) ? 1u : 0u);
+            }
         }
         out[base + pos] = perm[base + q];
     }
