@@ -113,6 +113,11 @@ CONFIGS = {
                    (electron(32, 0.0, 10 * _NC_C5), proton(32, 0.0, 10 * _NC_C5, colocate_with=0)),
                    steps=500, sort_every=20,
                    description="512x512x1024 laser-plasma slab z in [600,700), a0 = 10"),
+    # the paper's own benchmark: 40^3 grid,
+    # 50 particles per cell, 1000 steps, frozen plasma (zero momenta, zero fields;
+    # every stage still runs).  The paper's KNL time is 10.75 s = 3.36 ns/particle/step.
+    "FROZEN": Workload("FROZEN", 40, 40, 40, (electron(50, 0.0),), steps=1000, sort_every=20,
+                       description="paper frozen-plasma benchmark: 40^3, 50 ppc, u = 0, 1000 steps"),
     # small shapes for tests (not bench lines)
     "T_small": Workload("T_small", 8, 12, 16, (electron(4, 0.05),), steps=5, sort_every=2,
                         description="8x12x16 non-cubic test grid"),

@@ -430,3 +430,46 @@ def test_particles_on_faces_and_corners(pic, oracle_mod):
         gP, gi = sim.get_particles(0)
         pe, ue = compare_state(gP, gi, orc.P[0], orc.ids[0], _L(wl))
         assert max(field_errs(G, orc.F) + [pe, ue]) <= 1e-12
+
+
+@pytest.mark.slow
+def test_c3_full_size_two_species_sampled_and_continuity(pic, oracle_mod):
+    """C3 (128^3, 25 e + 25 p per cell, 104.9M particles) at full size in the
+    bench launch configuration, after 25 steps (one re-sort at step 20):
+    sampled particles of both species against the oracle's per-particle
+    gather / Boris / move on the GPU's own fields, and discrete charge
+    continuity of the GPU's deposit on the whole grid (oracle CIC rho)."""
+    from synth import get_config, gen_particles
+    wl = get_config("C3")
+    parts = gen_particles(wl)
+    sim = _sim(pic, wl)
+    _load(sim, parts)
+    del parts
+    sim.step(25)
+    F0 = sim.get_fields()
+    P0 = [sim.get_particles(s) for s in range(2)]
+    sim.step(1)
+    F1 = sim.get_fields()
+    P1 = [sim.get_particles(s) for s in range(2)]
+    orc = _oracle_for(oracle_mod, wl, [(np.zeros((6, 0)), np.zeros(0, np.uint64))] * 2)
+    orc.F[:] = F0
+    O = oracle_mod
+    L = np.array(_L(wl))
+    rng = np.random.default_rng(31)
+    for s, sp in enumerate(wl.species):
+        (A, ia), (B, ib) = P0[s], P1[s]
+        assert np.array_equal(ia, ib)            # no re-sort between the two states
+        for p in rng.choice(A.shape[1], 500, replace=False):
+            EB = orc.gather(*A[:3, p])
+            u = O.boris(sp.q, sp.m, wl.c, wl.dt, EB, A[3:, p])
+            xn = O.move(wl.c, wl.dt, u, A[:3, p])
+            xn = np.array([O.wrap(xn[d], L[d]) for d in range(3)])
+            assert rel_err(B[3:, p], u) <= TOL_STEP
+            d = (B[:3, p] - xn + L / 2) % L - L / 2
+            assert np.abs(d).max() <= TOL_STEP * L.max()
+    rho0 = sum(orc.rho_of(s, P0[s][0]) for s in range(2))
+    rho1 = sum(orc.rho_of(s, P1[s][0]) for s in range(2))
+    orc.F[6:] = F1[6:]
+    divj = orc.div_edge(6)
+    res = (rho1 - rho0) / wl.dt + divj
+    assert np.abs(res).max() <= 1e-12 * np.abs(divj).max() + 1e-15
