@@ -168,6 +168,39 @@ int pic_get_stage_times(pic_ctx *ctx, double ms[4], int64_t *particle_launches);
  * (counted on the host at enqueue time, graph nodes included); resets it. */
 int pic_get_launch_count(pic_ctx *ctx, int64_t *launches);
 
+/* Diagnostics of the state at step n (the
+ * quantities of SPEC.md:379-443), computed on the device over this rank's
+ * slab (sums and maxima are slab-local; the caller combines ranks):
+ *   rho^n(i,j,k) = sum_p q w S(x-i dx)S(y-j dy)S(z-k dz)/(dx dy dz) at nodes,
+ *     S the CIC hat (the charge the VB deposit conserves);
+ *   gauss = div E^n - 4 pi rho^n at nodes (backward differences);
+ *   continuity = (rho^n - rho^{n-1})/dt + div J^{n-1/2} at nodes;
+ *   div B^n at cell centres (forward differences).
+ * All fields are doubles; "max" fields are maxima of absolute values. */
+typedef struct pic_diag {
+    int64_t step;                           /* n */
+    double field_energy;                    /* sum (E^2 + B^2) dV / (8 pi) */
+    double kinetic_energy[PIC_MAX_SPECIES]; /* sum w m c^2 (gamma - 1), from u^{n-1/2} */
+    double charge;                          /* sum rho dV (= sum of q w of the live particles) */
+    double current[3];                      /* sum J^{n-1/2} dV per component */
+    double max_div_b;
+    double max_gauss;                       /* max |div E - 4 pi rho| */
+    double max_gauss_drift;                 /* max |gauss^n - gauss^{n0}|, n0 = the context's
+                                               first diagnostics call (0 at that call) */
+    double max_continuity;                  /* -1 unless the previous call was at step n-1 */
+} pic_diag;
+
+/* Computes *out (and, if rho != NULL, copies rho^n of the local slab without
+ * ghosts into the HOST array rho[nz_local][ny][nx]).  Collective when
+ * nranks > 1 (the top node plane of a slab belongs to the slab above; the
+ * Jz plane below is exchanged).  Enqueued on cfg->stream and synchronised;
+ * not part of the timed step. */
+int pic_diagnostics(pic_ctx *ctx, pic_diag *out, double *rho);
+
+/* The same for the n contexts of a PIC_FLAG_LOCAL_GROUP decomposition:
+ * out[r] (and rho[r], each may be NULL) for rank r. */
+int pic_diagnostics_group(pic_ctx *const *ctxs, int n, pic_diag *out, double *const *rho);
+
 /* Message for an error code / the last error of a context (never NULL). */
 const char *pic_strerror(int code);
 const char *pic_last_error(pic_ctx *ctx);

@@ -234,10 +234,12 @@ class Oracle:
     def field_energy(self):
         return lib().oracle_field_energy(C.byref(self._cfg), _p(self.F))
 
-    def kinetic_energy(self):
+    def kinetic_energy(self, species=None):
+        """sum w m c^2 (gamma - 1) over all species, or one species."""
+        sel = range(len(self.P)) if species is None else [species]
         return sum(lib().oracle_kinetic_energy(C.byref(self._cfg), s, self.P[s].shape[1],
                                                _p(self.P[s]))
-                   for s in range(len(self.P)))
+                   for s in sel)
 
 
 def boris(q, m, c, dt, EB, u):

@@ -78,4 +78,27 @@ struct SpeciesDev {
     MigrateDev mig;
 };
 
+// Periodic ghost images: f(p) for every padded index p in [-G, n+G)^3 that
+// is an image of interior cell (i,j,k) under the x/y periodicity (and z when
+// the slab is the whole box), the interior index included.
+// first periodic image index >= -G of i, stepping by n
+__device__ __forceinline__ int first_image(int i, int n)
+{
+    while (i - n >= -kGhost) i -= n;
+    return i;
+}
+
+template <class F>
+__device__ __forceinline__ void for_images(const GridDev &g, int i, int j, int k, F &&f)
+{
+    const int i0 = first_image(i, g.nx), j0 = first_image(j, g.ny);
+    const int k0 = g.periodic_z_local ? first_image(k, g.nz) : k;
+    const int kend = g.periodic_z_local ? g.nz + kGhost : k + 1;
+    const int kstep = g.periodic_z_local ? g.nz : 1;
+    for (int kk = k0; kk < kend; kk += kstep)
+        for (int jj = j0; jj < g.ny + kGhost; jj += g.ny)
+            for (int ii = i0; ii < g.nx + kGhost; ii += g.nx)
+                f(pidx(g, ii, jj, kk));
+}
+
 }  // namespace pic

@@ -70,4 +70,18 @@ void launch_mig_finalize(const MigrateDev &m, unsigned *err, cudaStream_t st);
 void launch_mig_append(const double *recv0, const double *recv1, int cap, const ParticlesDev &P,
                        int64_t *dev_n, int64_t pcap, unsigned *err, cudaStream_t st);
 
+// ---- diag.cu : diagnostics between steps ----
+// CIC rho of live particles [0, *dev_n) into the padded node array `rho`
+// (pre-zeroed; the top ghost plane holds what belongs to the slab above) and
+// sum (gamma - 1) into *acc_kinetic.
+void launch_diag_particles(const GridDev &g, const ParticlesDev &P, const int64_t *dev_n, int64_t cap,
+                           double qw, double *rho, double *acc_kinetic, cudaStream_t st);
+// folds rho (+ rho_below: the lower slab's top ghost plane, or nullptr), then
+// per node: energies, sums, div B, Gauss residual and drift vs gauss0
+// (stored instead when !have_g0), continuity vs rho_prev (then rho_prev = rho).
+// jz_below: the lower slab's top interior Jz plane (nullptr when periodic).
+void launch_diag_nodes(const GridDev &g, const double *EB, const double *J, const double *jz_below,
+                       double *rho, const double *rho_below, double *rho_prev, double *gauss0,
+                       bool have_prev, bool have_g0, double *acc, cudaStream_t st);
+
 }  // namespace pic

@@ -40,6 +40,7 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 constexpr int64_t kDefaultMigrate = 65536;
+constexpr int kAccSlots = 16;   // diagnostics accumulators, see k_diag_nodes
 
 struct Layout {
     GridDev g{};
@@ -52,6 +53,7 @@ struct Layout {
            off_bsums = 0, off_err = 0, off_stat = 0, off_n = 0;
     size_t off_msend[PIC_MAX_SPECIES][2] = {}, off_mrecv[PIC_MAX_SPECIES][2] = {}, off_mcnt = 0;
     size_t off_jrecv[2] = {};
+    size_t off_rho = 0, off_rho_prev = 0, off_gauss0 = 0, off_acc = 0;   // diagnostics
     size_t total = 0;
 };
 
@@ -148,6 +150,10 @@ Layout make_layout(const pic_config *c)
     L.off_stat = o; o = align_up(o + 2 * PIC_MAX_SPECIES * sizeof(unsigned));
     L.off_n = o; o = align_up(o + PIC_MAX_SPECIES * sizeof(int64_t));
     L.off_mcnt = o; o = align_up(o + 2 * PIC_MAX_SPECIES * sizeof(unsigned));
+    L.off_rho = o; o = align_up(o + sizeof(double) * (size_t)g.cs);
+    L.off_rho_prev = o; o = align_up(o + sizeof(double) * (size_t)g.cs);
+    L.off_gauss0 = o; o = align_up(o + sizeof(double) * (size_t)g.cs);
+    L.off_acc = o; o = align_up(o + sizeof(double) * kAccSlots);
     L.total = o;
     return L;
 }
@@ -256,6 +262,10 @@ struct pic_ctx {
     MigrateDev mig[PIC_MAX_SPECIES];
     double *mrecv[PIC_MAX_SPECIES][2] = {};
     double *jrecv[2] = {nullptr, nullptr};     // [from rank-1, from rank+1]
+    // diagnostics (diag.cu): padded node arrays and accumulators
+    double *rho = nullptr, *rho_prev = nullptr, *gauss0 = nullptr, *acc = nullptr;
+    int64_t diag_last_step = -2;
+    bool diag_have_g0 = false;
     int64_t step_index = 0;
     bool use_tile = false;     // fused supercell kernel (else the naive kernel)
     bool slabs = false;        // nranks > 1
@@ -582,6 +592,73 @@ void collect_profile(pic_ctx *ctx)
     ctx->ev_used = 0;
 }
 
+// ---- diagnostics (diag.cu); between steps, so jrecv is free scratch ----
+double *diag_rho_below(pic_ctx *ctx) { return ctx->jrecv[0]; }
+double *diag_jz_below(pic_ctx *ctx) { return ctx->jrecv[0] + plane_pair(ctx->L.g); }
+
+// the top ghost node pair of rho (charge of nodes owned by the slab above)
+// and the top interior Jz pair go up
+std::vector<Msg> msgs_diag(pic_ctx *ctx)
+{
+    const GridDev &g = ctx->L.g;
+    const double *Jz = ctx->J[ctx->jlast] + 2 * g.cs;
+    return {{ctx->rho + plane_off(g, g.nz), diag_rho_below(ctx), plane_pair(g), 1},
+            {(double *)Jz + plane_off(g, g.nz - 2), diag_jz_below(ctx), plane_pair(g), 1}};
+}
+
+int diag_particles(pic_ctx *ctx)
+{
+    const GridDev &g = ctx->L.g;
+    PIC_CUDA(ctx, cudaMemsetAsync(ctx->rho, 0, sizeof(double) * (size_t)g.cs, ctx->st));
+    PIC_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, sizeof(double) * kAccSlots, ctx->st));
+    for (int s = 0; s < ctx->cfg.n_species; ++s) {
+        launch_diag_particles(g, ctx->A[s], ctx->dev_n + s, ctx->L.cap[s], ctx->cfg.q[s] * ctx->cfg.w[s],
+                              ctx->rho, ctx->acc + 9 + s, ctx->st);
+        ctx->launches += 2;
+    }
+    PIC_CUDA(ctx, cudaGetLastError());
+    return PIC_OK;
+}
+
+int diag_nodes(pic_ctx *ctx, pic_diag *out, double *rho_host)
+{
+    const GridDev &g = ctx->L.g;
+    const bool have_prev = ctx->diag_last_step == ctx->step_index - 1;
+    launch_diag_nodes(g, ctx->EB, ctx->J[ctx->jlast], ctx->slabs ? diag_jz_below(ctx) + (size_t)g.X * g.Y : nullptr,
+                      ctx->rho, ctx->slabs ? diag_rho_below(ctx) : nullptr, ctx->rho_prev, ctx->gauss0,
+                      have_prev, ctx->diag_have_g0, ctx->acc, ctx->st);
+    ctx->launches += 2;
+    PIC_CUDA(ctx, cudaGetLastError());
+    double a[kAccSlots];
+    PIC_CUDA(ctx, cudaMemcpyAsync(a, ctx->acc, sizeof(a), cudaMemcpyDeviceToHost, ctx->st));
+    if (rho_host) {
+        cudaMemcpy3DParms p = {};
+        p.srcPtr = make_cudaPitchedPtr((void *)ctx->rho, sizeof(double) * g.X, g.X, g.Y);
+        p.srcPos = make_cudaPos(sizeof(double) * kGhost, kGhost, kGhost);
+        p.dstPtr = make_cudaPitchedPtr(rho_host, sizeof(double) * g.nx, g.nx, g.ny);
+        p.extent = make_cudaExtent(sizeof(double) * g.nx, g.ny, g.nz);
+        p.kind = cudaMemcpyDeviceToHost;
+        PIC_CUDA(ctx, cudaMemcpy3DAsync(&p, ctx->st));
+    }
+    PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    const double dV = g.dx * g.dy * g.dz;
+    pic_diag d{};
+    d.step = ctx->step_index;
+    d.field_energy = a[0] * dV / (8.0 * M_PI);
+    for (int s = 0; s < PIC_MAX_SPECIES; ++s)
+        d.kinetic_energy[s] = s < ctx->cfg.n_species ? a[9 + s] * ctx->cfg.w[s] * ctx->cfg.m[s] * g.c * g.c : 0.0;
+    d.charge = a[1] * dV;
+    for (int c = 0; c < 3; ++c) d.current[c] = a[2 + c] * dV;
+    d.max_div_b = a[5];
+    d.max_gauss = a[6];
+    d.max_gauss_drift = ctx->diag_have_g0 ? a[7] : 0.0;
+    d.max_continuity = have_prev ? a[8] : -1.0;
+    ctx->diag_have_g0 = true;
+    ctx->diag_last_step = ctx->step_index;
+    if (out) *out = d;
+    return PIC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -651,6 +728,10 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->sort.start = (uint32_t *)(ctx->ws + L.off_start);
     ctx->sort.block_sums = (uint32_t *)(ctx->ws + L.off_bsums);
     ctx->err = (unsigned *)(ctx->ws + L.off_err);
+    ctx->rho = (double *)(ctx->ws + L.off_rho);
+    ctx->rho_prev = (double *)(ctx->ws + L.off_rho_prev);
+    ctx->gauss0 = (double *)(ctx->ws + L.off_gauss0);
+    ctx->acc = (double *)(ctx->ws + L.off_acc);
     ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell);
     configure_tile_kernels();
     {
@@ -937,6 +1018,51 @@ int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps)
         if (e != PIC_OK && rc == PIC_OK) rc = e;
     }
     return rc;
+}
+
+int pic_diagnostics(pic_ctx *ctx, pic_diag *out, double *rho)
+{
+    if (!ctx) return PIC_EINVAL;
+    if (ctx->local_group) return fail(ctx, PIC_ESTATE, "PIC_FLAG_LOCAL_GROUP contexts use pic_diagnostics_group");
+    if (ctx->ghosts_stale) {
+        int rc = exchange_nccl(ctx, msgs_fields(ctx, 0, 6));
+        if (rc != PIC_OK) return rc;
+        ctx->ghosts_stale = false;
+    }
+    int rc = diag_particles(ctx);
+    if (rc == PIC_OK && ctx->slabs) rc = exchange_nccl(ctx, msgs_diag(ctx));
+    if (rc == PIC_OK) rc = diag_nodes(ctx, out, rho);
+    return rc;
+}
+
+int pic_diagnostics_group(pic_ctx *const *ctxs, int n, pic_diag *out, double *const *rho)
+{
+    if (!ctxs || n < 1) return PIC_EINVAL;
+    for (int r = 0; r < n; ++r) {
+        if (!ctxs[r] || !ctxs[r]->local_group || ctxs[r]->cfg.nranks != n || ctxs[r]->cfg.rank != r)
+            return fail(ctxs[r], PIC_EINVAL, "pic_diagnostics_group needs PIC_FLAG_LOCAL_GROUP ranks 0..n-1");
+    }
+    auto all = [&](auto f) {
+        std::vector<std::vector<Msg>> m(n);
+        for (int r = 0; r < n; ++r) m[r] = f(ctxs[r]);
+        return m;
+    };
+    if (ctxs[0]->ghosts_stale) {
+        int rc = exchange_local(ctxs, n, all([](pic_ctx *c) { return msgs_fields(c, 0, 6); }));
+        if (rc != PIC_OK) return rc;
+        for (int r = 0; r < n; ++r) ctxs[r]->ghosts_stale = false;
+    }
+    for (int r = 0; r < n; ++r) {
+        int rc = diag_particles(ctxs[r]);
+        if (rc != PIC_OK) return rc;
+    }
+    int rc = exchange_local(ctxs, n, all([](pic_ctx *c) { return msgs_diag(c); }));
+    if (rc != PIC_OK) return rc;
+    for (int r = 0; r < n; ++r) {
+        rc = diag_nodes(ctxs[r], out ? out + r : nullptr, rho ? rho[r] : nullptr);
+        if (rc != PIC_OK) return rc;
+    }
+    return PIC_OK;
 }
 
 int pic_get_stage_times(pic_ctx *ctx, double ms[4], int64_t *particle_launches)

@@ -31,7 +31,8 @@ EXPORTS = [
     "pic_workspace_size", "pic_init", "pic_set_particles", "pic_set_fields", "pic_step",
     "pic_get_fields", "pic_get_particles", "pic_get_count", "pic_get_step_index",
     "pic_get_stage_times", "pic_get_launch_count", "pic_strerror", "pic_last_error",
-    "pic_destroy", "pic_nccl_unique_id", "pic_step_group",
+    "pic_destroy", "pic_nccl_unique_id", "pic_step_group", "pic_diagnostics",
+    "pic_diagnostics_group",
 ]
 
 
@@ -53,6 +54,28 @@ class PicConfig(C.Structure):
         ("nccl_id", C.c_uint8 * 128),
         ("stream", C.c_void_p),
     ]
+
+
+class PicDiag(C.Structure):
+    """pic_diag (include/pic.h): slab-local diagnostics at step n."""
+    _fields_ = [
+        ("step", C.c_int64),
+        ("field_energy", C.c_double),
+        ("kinetic_energy", C.c_double * MAX_SPECIES),
+        ("charge", C.c_double),
+        ("current", C.c_double * 3),
+        ("max_div_b", C.c_double),
+        ("max_gauss", C.c_double),
+        ("max_gauss_drift", C.c_double),
+        ("max_continuity", C.c_double),
+    ]
+
+    def as_dict(self, n_species=MAX_SPECIES):
+        return {"step": self.step, "field_energy": self.field_energy,
+                "kinetic_energy": list(self.kinetic_energy)[:n_species], "charge": self.charge,
+                "current": list(self.current), "max_div_b": self.max_div_b,
+                "max_gauss": self.max_gauss, "max_gauss_drift": self.max_gauss_drift,
+                "max_continuity": self.max_continuity}
 
 
 class PicError(RuntimeError):
@@ -92,6 +115,9 @@ def lib():
         L.pic_destroy.restype = None
         L.pic_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
         L.pic_step_group.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int64]
+        L.pic_diagnostics.argtypes = [C.c_void_p, C.POINTER(PicDiag), dp]
+        L.pic_diagnostics_group.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(PicDiag),
+                                            C.POINTER(dp)]
         for name in EXPORTS:
             if name not in ("pic_strerror", "pic_last_error", "pic_destroy"):
                 getattr(L, name).restype = C.c_int
@@ -150,6 +176,7 @@ class Simulation:
             self._check(L.pic_init(C.byref(cfg), C.c_void_p(aligned), nbytes.value, C.byref(self.ctx)),
                         None)
         self.nx, self.ny, self.nz_local = cfg.nx, cfg.ny, cfg.nz // cfg.nranks
+        self.n_species = cfg.n_species
 
     def _check(self, rc, ctx="self"):
         if rc != PIC_OK:
@@ -197,6 +224,16 @@ class Simulation:
                                             *[_dptr(P[i]) for i in range(6)],
                                             ids.ctypes.data_as(C.POINTER(C.c_uint64))))
         return P[:, :cap.value], ids[:cap.value]
+
+    def diagnostics(self, rho=False):
+        """pic_diagnostics: dict of slab-local diagnostics (+ rho^n array if rho)."""
+        d = PicDiag()
+        r = np.empty((self.nz_local, self.ny, self.nx), dtype=np.float64) if rho else None
+        self._check(lib().pic_diagnostics(self.ctx, C.byref(d), _dptr(r)))
+        out = d.as_dict(self.n_species)
+        if rho:
+            out["rho"] = r
+        return out
 
     def step_index(self):
         n = C.c_int64(0)
@@ -276,6 +313,24 @@ def broadcast_nccl_id(id_bytes, group=None) -> bytes:
         t.copy_(torch.frombuffer(bytearray(id_bytes), dtype=torch.uint8))
     dist.broadcast(t, src=0, group=group)
     return bytes(t.cpu().tolist())
+
+
+def diagnostics_group(sims, rho=False):
+    """pic_diagnostics_group over PIC_FLAG_LOCAL_GROUP slab Simulations: list of dicts."""
+    n = len(sims)
+    arr = (C.c_void_p * n)(*[s.ctx.value for s in sims])
+    ds = (PicDiag * n)()
+    rs = [np.empty((s.nz_local, s.ny, s.nx), dtype=np.float64) for s in sims] if rho else None
+    rp = (C.POINTER(C.c_double) * n)(*[_dptr(r) for r in rs]) if rho else None
+    rc = lib().pic_diagnostics_group(arr, n, ds, rp)
+    if rc != PIC_OK:
+        msgs = "; ".join(lib().pic_last_error(s.ctx).decode() for s in sims)
+        raise PicError(rc, msgs)
+    out = [ds[r].as_dict(sims[r].n_species) for r in range(n)]
+    if rho:
+        for r in range(n):
+            out[r]["rho"] = rs[r]
+    return out
 
 
 def step_group(sims, nsteps=1):

@@ -49,21 +49,23 @@ def test_oracle_exports_its_header(oracle_mod):
         assert hasattr(L, n), n
 
 
-def test_config_layout_matches_c(tmp_path):
-    from paper_1608_01009_b200.pic import PicConfig
-    fields = [f for f, _ in PicConfig._fields_]
+@pytest.mark.parametrize("cname, pyname", [("pic_config", "PicConfig"), ("pic_diag", "PicDiag")])
+def test_struct_layout_matches_c(tmp_path, cname, pyname):
+    from paper_1608_01009_b200 import pic
+    T = getattr(pic, pyname)
+    fields = [f for f, _ in T._fields_]
     prog = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"',
-            "int main(void){", 'printf("%zu\\n", sizeof(pic_config));']
-    prog += [f'printf("%zu\\n", offsetof(pic_config, {f}));' for f in fields]
+            "int main(void){", f'printf("%zu\\n", sizeof({cname}));']
+    prog += [f'printf("%zu\\n", offsetof({cname}, {f}));' for f in fields]
     prog += ["return 0;}"]
     src = tmp_path / "layout.c"
     src.write_text("\n".join(prog))
     exe = tmp_path / "layout"
     subprocess.check_call(["gcc", "-o", str(exe), str(src)])
     vals = [int(v) for v in subprocess.check_output([str(exe)]).split()]
-    assert vals[0] == C.sizeof(PicConfig)
+    assert vals[0] == C.sizeof(T)
     for f, off in zip(fields, vals[1:]):
-        assert getattr(PicConfig, f).offset == off, f
+        assert getattr(T, f).offset == off, f
 
 
 def _cfg(**kw):
