@@ -33,7 +33,14 @@ class OracleConfig(C.Structure):
         ("w", C.c_double * MAX_SPECIES),
         ("supercell", C.c_int64),
         ("sort_every", C.c_int64),
+        ("bc_z", C.c_int64),
+        ("laser_e0", C.c_double), ("laser_omega", C.c_double), ("laser_ramp", C.c_double),
+        ("laser_t0", C.c_double), ("laser_pol_x", C.c_double), ("laser_pol_y", C.c_double),
     ]
+
+
+BC_PERIODIC = 0
+BC_OPEN = 1
 
 
 def build(force: bool = False) -> str:
@@ -69,8 +76,11 @@ def lib():
         L.oracle_sort_key.restype = C.c_int64
         L.oracle_sort.argtypes = [cp, C.c_int64, _dp, _u64p]
         L.oracle_b_half.argtypes = [cp, _dp]
-        L.oracle_e_full.argtypes = [cp, _dp]
-        L.oracle_push_species.argtypes = [cp, _dp, C.c_int, C.c_int64, _dp]
+        L.oracle_e_full.argtypes = [cp, _dp, C.c_int64]
+        L.oracle_laser.argtypes = [cp, C.c_double, C.c_double]
+        L.oracle_laser.restype = C.c_double
+        L.oracle_laser_preload.argtypes = [cp, _dp]
+        L.oracle_push_species.argtypes = [cp, _dp, C.c_int, C.POINTER(C.c_int64), _dp, _u64p]
         L.oracle_push_species.restype = C.c_int
         L.oracle_step.argtypes = [cp, _dp, C.POINTER(C.c_int64), C.POINTER(_dp),
                                   C.POINTER(_u64p), C.c_int64]
@@ -115,6 +125,13 @@ class Grid:
     species: list = field(default_factory=list)
     supercell: int = 4
     sort_every: int = 20
+    # NEXT-1 (reading R21): open z boundaries and the incident laser
+    bc_z: int = BC_PERIODIC
+    laser_e0: float = 0.0
+    laser_omega: float = 0.0
+    laser_ramp: float = 0.0
+    laser_t0: float = 0.0
+    laser_pol: tuple = (1.0, 0.0)
 
     def cfg(self) -> OracleConfig:
         c = OracleConfig()
@@ -126,6 +143,10 @@ class Grid:
             c.q[i], c.m[i], c.w[i] = s.q, s.m, s.w
         c.supercell = self.supercell
         c.sort_every = self.sort_every
+        c.bc_z = self.bc_z
+        c.laser_e0, c.laser_omega, c.laser_ramp, c.laser_t0 = (
+            self.laser_e0, self.laser_omega, self.laser_ramp, self.laser_t0)
+        c.laser_pol_x, c.laser_pol_y = self.laser_pol
         return c
 
     @property
@@ -170,7 +191,22 @@ class Oracle:
             rc = L.oracle_step(C.byref(self._cfg), _p(self.F), counts, Pp, Ip, self.step_index)
             if rc != 0:
                 raise RuntimeError(f"oracle_step failed with code {rc}")
+            self._shrink(list(counts)[:ns])
             self.step_index += 1
+
+    def _shrink(self, counts):
+        # open z: the C side removed particles in place, rows now have stride m
+        for s, m in enumerate(counts):
+            n = self.P[s].shape[1]
+            if m != n:
+                self.P[s] = self.P[s].reshape(-1)[:6 * m].reshape(6, m).copy()
+                self.ids[s] = self.ids[s][:m].copy()
+
+    def laser_preload(self):
+        lib().oracle_laser_preload(C.byref(self._cfg), _p(self.F))
+
+    def laser(self, z, t):
+        return lib().oracle_laser(C.byref(self._cfg), z, t)
 
     # ---- single-operation entry points (pins) ----
     def gather(self, x, y, z):
@@ -186,14 +222,19 @@ class Oracle:
     def b_half(self):
         lib().oracle_b_half(C.byref(self._cfg), _p(self.F))
 
-    def e_full(self):
-        lib().oracle_e_full(C.byref(self._cfg), _p(self.F))
+    def e_full(self, step=None):
+        lib().oracle_e_full(C.byref(self._cfg), _p(self.F),
+                            self.step_index if step is None else step)
 
     def push_species(self, s):
-        rc = lib().oracle_push_species(C.byref(self._cfg), _p(self.F), s,
-                                       self.P[s].shape[1], _p(self.P[s]))
+        n = C.c_int64(self.P[s].shape[1])
+        rc = lib().oracle_push_species(C.byref(self._cfg), _p(self.F), s, C.byref(n),
+                                       _p(self.P[s]), _p(self.ids[s]))
         if rc != 0:
             raise RuntimeError(f"oracle_push_species failed with code {rc}")
+        counts = [p.shape[1] for p in self.P]
+        counts[s] = n.value
+        self._shrink(counts)
 
     def sort_keys(self, P):
         cfg = C.byref(self._cfg)

@@ -28,6 +28,14 @@ static int64_t cell_index(const oracle_config *cfg, int64_t i, int64_t j, int64_
            cfg->nx * (wrap_index(j, cfg->ny) + cfg->ny * wrap_index(k, cfg->nz));
 }
 
+/* NEXT-1 (reading R21): with an open z boundary the grid has no z images;
+ * a node index outside [0, nz) lies outside the box (fields read 0 there,
+ * deposits there are dropped). */
+static int z_outside(const oracle_config *cfg, int64_t k)
+{
+    return cfg->bc_z == ORACLE_BC_OPEN && (k < 0 || k >= cfg->nz);
+}
+
 /* Yee staggering, in cell units:
  * Ex (i+1/2,j,k), Ey (i,j+1/2,k), Ez (i,j,k+1/2),
  * Bx (i,j+1/2,k+1/2), By (i+1/2,j,k+1/2), Bz (i+1/2,j+1/2,k). */
@@ -63,7 +71,9 @@ void oracle_gather(const oracle_config *cfg, const double *F,
             for (int b = 0; b < 2; ++b)
                 for (int a = 0; a < 2; ++a)
                     sum += W[0][a] * W[1][b] * W[2][c] *
-                           Fc[cell_index(cfg, i0[0] + a, i0[1] + b, i0[2] + c)];
+                           (z_outside(cfg, i0[2] + c)
+                                ? 0.0
+                                : Fc[cell_index(cfg, i0[0] + a, i0[1] + b, i0[2] + c)]);
         out[comp] = sum;
     }
 }
@@ -140,12 +150,15 @@ static void deposit_segment(const oracle_config *cfg, double qw,
     for (int p = 0; p < 2; ++p) {
         for (int r = 0; r < 2; ++r) {
             const double s = (p == r) ? 1.0 : -1.0;
-            J[0 * N + cell_index(cfg, cell[0], cell[1] + p, cell[2] + r)] +=
-                fx * (W[1][p] * W[2][r] + s * cxx);
-            J[1 * N + cell_index(cfg, cell[0] + p, cell[1], cell[2] + r)] +=
-                fy * (W[0][p] * W[2][r] + s * cyy);
-            J[2 * N + cell_index(cfg, cell[0] + p, cell[1] + r, cell[2])] +=
-                fz * (W[0][p] * W[1][r] + s * czz);
+            if (!z_outside(cfg, cell[2] + r))
+                J[0 * N + cell_index(cfg, cell[0], cell[1] + p, cell[2] + r)] +=
+                    fx * (W[1][p] * W[2][r] + s * cxx);
+            if (!z_outside(cfg, cell[2] + r))
+                J[1 * N + cell_index(cfg, cell[0] + p, cell[1], cell[2] + r)] +=
+                    fy * (W[0][p] * W[2][r] + s * cyy);
+            if (!z_outside(cfg, cell[2]))
+                J[2 * N + cell_index(cfg, cell[0] + p, cell[1] + r, cell[2])] +=
+                    fz * (W[0][p] * W[1][r] + s * czz);
         }
     }
 }
@@ -322,8 +335,12 @@ void oracle_b_half(const oracle_config *cfg, double *F)
                 double cx = (Ez[yp] - Ez[o]) / cfg->dy - (Ey[zp] - Ey[o]) / cfg->dz;
                 double cy = (Ex[zp] - Ex[o]) / cfg->dz - (Ez[xp] - Ez[o]) / cfg->dx;
                 double cz = (Ey[xp] - Ey[o]) / cfg->dx - (Ex[yp] - Ex[o]) / cfg->dy;
-                Bx[o] = Bx[o] - k * cx;
-                By[o] = By[o] - k * cy;
+                /* open z: Bx, By of the top plane sit at z = (nz - 1/2) dz,
+                 * outside the box [0, (nz-1) dz]; they are not advanced */
+                if (!(cfg->bc_z == ORACLE_BC_OPEN && kk == nz - 1)) {
+                    Bx[o] = Bx[o] - k * cx;
+                    By[o] = By[o] - k * cy;
+                }
                 Bz[o] = Bz[o] - k * cz;
             }
 }
@@ -331,7 +348,7 @@ void oracle_b_half(const oracle_config *cfg, double *F)
 /* a7 / O3 -- E += c dt curl B - 4 pi dt J, curl B evaluated at the E
  * locations with backward differences (SPEC.md:82
  * Gaussian units, reading R3). */
-void oracle_e_full(const oracle_config *cfg, double *F)
+void oracle_e_full(const oracle_config *cfg, double *F, int64_t step_index)
 {
     const int64_t nx = cfg->nx, ny = cfg->ny, nz = cfg->nz, N = nx * ny * nz;
     double *Ex = F, *Ey = F + N, *Ez = F + 2 * N;
@@ -339,6 +356,17 @@ void oracle_e_full(const oracle_config *cfg, double *F)
     const double *Jx = F + 6 * N, *Jy = F + 7 * N, *Jz = F + 8 * N;
     const double k = cfg->c * cfg->dt;
     const double kj = 4.0 * M_PI * cfg->dt;
+    const int open = cfg->bc_z == ORACLE_BC_OPEN;
+    const int64_t P = nx * ny;   /* one z plane */
+    double *old = NULL;          /* open z: Ex, Ey of planes 0, 1, nz-2, nz-1 at time n */
+    if (open) {
+        old = (double *)malloc(sizeof(double) * 8 * (size_t)P);
+        const int64_t planes[4] = {0, 1, nz - 2, nz - 1};
+        for (int q = 0; q < 4; ++q) {
+            memcpy(old + (2 * q) * P, Ex + planes[q] * P, sizeof(double) * (size_t)P);
+            memcpy(old + (2 * q + 1) * P, Ey + planes[q] * P, sizeof(double) * (size_t)P);
+        }
+    }
     for (int64_t kk = 0; kk < nz; ++kk)
         for (int64_t j = 0; j < ny; ++j)
             for (int64_t i = 0; i < nx; ++i) {
@@ -349,19 +377,86 @@ void oracle_e_full(const oracle_config *cfg, double *F)
                 double cx = (Bz[o] - Bz[ym]) / cfg->dy - (By[o] - By[zm]) / cfg->dz;
                 double cy = (Bx[o] - Bx[zm]) / cfg->dz - (Bz[o] - Bz[xm]) / cfg->dx;
                 double cz = (By[o] - By[xm]) / cfg->dx - (Bx[o] - Bx[ym]) / cfg->dy;
-                Ex[o] = Ex[o] + k * cx - kj * Jx[o];
-                Ey[o] = Ey[o] + k * cy - kj * Jy[o];
-                Ez[o] = Ez[o] + k * cz - kj * Jz[o];
+                /* open z: Ex, Ey of planes 0 and nz-1 come from the boundary
+                 * condition below; Ez of the top plane (z = (nz - 1/2) dz) lies
+                 * outside the box and is not advanced */
+                if (!(open && (kk == 0 || kk == nz - 1))) {
+                    Ex[o] = Ex[o] + k * cx - kj * Jx[o];
+                    Ey[o] = Ey[o] + k * cy - kj * Jy[o];
+                }
+                if (!(open && kk == nz - 1))
+                    Ez[o] = Ez[o] + k * cz - kj * Jz[o];
             }
+    if (open) {
+        /* first-order Mur (one-way wave equation along the normal) on the
+         * scattered field E - E_inc at z = 0 and on E at z = (nz-1) dz:
+         *   E0^{n+1} = I0^{n+1} + (E1^n - I1^n) + a ((E1^{n+1} - I1^{n+1}) - (E0^n - I0^n))
+         *   EK^{n+1} = E(K-1)^n + a (E(K-1)^{n+1} - EK^n),   a = (c dt - dz)/(c dt + dz),
+         * I_k^n = pol E_inc(k dz, n dt) (reading R21). */
+        const double a = (cfg->c * cfg->dt - cfg->dz) / (cfg->c * cfg->dt + cfg->dz);
+        const double t0 = (double)step_index * cfg->dt, t1 = (double)(step_index + 1) * cfg->dt;
+        const double i00 = oracle_laser(cfg, 0.0, t0), i01 = oracle_laser(cfg, 0.0, t1);
+        const double i10 = oracle_laser(cfg, cfg->dz, t0), i11 = oracle_laser(cfg, cfg->dz, t1);
+        const double pol[2] = {cfg->laser_pol_x, cfg->laser_pol_y};
+        double *E[2] = {Ex, Ey};
+        for (int c = 0; c < 2; ++c)
+            for (int64_t q = 0; q < P; ++q) {
+                const double e0o = old[(0 + c) * P + q], e1o = old[(2 + c) * P + q];
+                const double eKm1o = old[(4 + c) * P + q], eKo = old[(6 + c) * P + q];
+                const double e1n = E[c][1 * P + q], eKm1n = E[c][(nz - 2) * P + q];
+                E[c][0 * P + q] = pol[c] * i01 + (e1o - pol[c] * i10) +
+                                  a * ((e1n - pol[c] * i11) - (e0o - pol[c] * i00));
+                E[c][(nz - 1) * P + q] = eKm1o + a * (eKm1n - eKo);
+            }
+        free(old);
+    }
+}
+
+/* NEXT-1 -- the incident plane wave of BASELINE.json configs[4] ("a
+ * linearly polarised plane wave of normalised amplitude a0 ... injected from
+ * z=0"; reading R21): E_inc(z, t) = E0 env(xi) sin(omega xi),
+ * xi = t + t0 - z / c. */
+double oracle_laser(const oracle_config *cfg, double z, double t)
+{
+    const double xi = t + cfg->laser_t0 - z / cfg->c;
+    if (!(xi > 0.0))
+        return 0.0;
+    double env = 1.0;
+    if (xi < cfg->laser_ramp) {
+        const double sr = sin(M_PI * xi / (2.0 * cfg->laser_ramp));
+        env = sr * sr;
+    }
+    return cfg->laser_e0 * env * sin(cfg->laser_omega * xi);
+}
+
+void oracle_laser_preload(const oracle_config *cfg, double *F)
+{
+    const int64_t nx = cfg->nx, ny = cfg->ny, nz = cfg->nz, N = nx * ny * nz, P = nx * ny;
+    memset(F, 0, sizeof(double) * 6 * (size_t)N);
+    for (int64_t kk = 0; kk < nz; ++kk) {
+        const double e = oracle_laser(cfg, (double)kk * cfg->dz, 0.0);
+        const double b = kk < nz - 1 ? oracle_laser(cfg, ((double)kk + 0.5) * cfg->dz, 0.0) : 0.0;
+        for (int64_t q = 0; q < P; ++q) {
+            F[0 * N + kk * P + q] = cfg->laser_pol_x * e;
+            F[1 * N + kk * P + q] = cfg->laser_pol_y * e;
+            F[3 * N + kk * P + q] = -cfg->laser_pol_y * b;
+            F[4 * N + kk * P + q] = cfg->laser_pol_x * b;
+        }
+    }
 }
 
 /* O2 step 2 for one species, particles in array order:
  * gather E^n,B^n -> Boris -> move -> VB deposit x -> x' -> wrap x'. */
 int oracle_push_species(const oracle_config *cfg, double *F, int species,
-                        int64_t n, double *P)
+                        int64_t *n_io, double *P, uint64_t *id)
 {
     const double q = cfg->q[species], m = cfg->m[species], w = cfg->w[species];
     const double L[3] = {cfg->nx * cfg->dx, cfg->ny * cfg->dy, cfg->nz * cfg->dz};
+    const int open = cfg->bc_z == ORACLE_BC_OPEN;
+    const double zmax = (double)(cfg->nz - 1) * cfg->dz;   /* open z: particles live in [0, zmax) */
+    const int64_t n = *n_io;
+    unsigned char *gone = open ? (unsigned char *)calloc((size_t)(n > 0 ? n : 1), 1) : NULL;
+    int64_t kept = n;
     for (int64_t p = 0; p < n; ++p) {
         double x[3] = {P[p], P[n + p], P[2 * n + p]};
         double u[3] = {P[3 * n + p], P[4 * n + p], P[5 * n + p]};
@@ -370,13 +465,35 @@ int oracle_push_species(const oracle_config *cfg, double *F, int species,
         oracle_boris(q, m, cfg->c, cfg->dt, EB, u);
         oracle_move(cfg->c, cfg->dt, u, x, xn);
         int rc = oracle_deposit_vb(cfg, q * w, x, xn, F);
-        if (rc != ORACLE_OK)
+        if (rc != ORACLE_OK) {
+            free(gone);
             return rc;
+        }
         for (int d = 0; d < 3; ++d) {
-            P[d * n + p] = oracle_wrap(xn[d], L[d]);
+            P[d * n + p] = (open && d == 2) ? xn[d] : oracle_wrap(xn[d], L[d]);
             P[(3 + d) * n + p] = u[d];
         }
+        if (open && !(xn[2] >= 0.0 && xn[2] < zmax)) {   /* left through an open face */
+            gone[p] = 1;
+            --kept;
+        }
     }
+    if (open && kept < n) {
+        /* remove in place, keeping the order; rows move to stride `kept`
+         * (every write index is <= its read index, so nothing unread is overwritten) */
+        for (int c = 0; c < 6; ++c) {
+            int64_t k = 0;
+            for (int64_t p = 0; p < n; ++p)
+                if (!gone[p])
+                    P[c * kept + k++] = P[c * n + p];
+        }
+        int64_t k = 0;
+        for (int64_t p = 0; p < n; ++p)
+            if (!gone[p])
+                id[k++] = id[p];
+    }
+    free(gone);
+    *n_io = kept;
     return ORACLE_OK;
 }
 
@@ -386,7 +503,7 @@ int oracle_push_species(const oracle_config *cfg, double *F, int species,
  *   2. zero J; per species, per particle: gather, Boris, move, deposit, wrap;
  *   3. B half-step with E^n; 4. E full step with B^{n+1/2} and J^{n+1/2};
  *   5. B half-step with E^{n+1}. */
-int oracle_step(const oracle_config *cfg, double *F, const int64_t *counts,
+int oracle_step(const oracle_config *cfg, double *F, int64_t *counts,
                 double *const *P, uint64_t *const *ids, int64_t step_index)
 {
     const int64_t N = cfg->nx * cfg->ny * cfg->nz;
@@ -395,12 +512,12 @@ int oracle_step(const oracle_config *cfg, double *F, const int64_t *counts,
             oracle_sort(cfg, counts[s], P[s], ids[s]);
     memset(F + 6 * N, 0, sizeof(double) * 3 * (size_t)N);
     for (int s = 0; s < cfg->n_species; ++s) {
-        int rc = oracle_push_species(cfg, F, s, counts[s], P[s]);
+        int rc = oracle_push_species(cfg, F, s, &counts[s], P[s], ids[s]);
         if (rc != ORACLE_OK)
             return rc;
     }
     oracle_b_half(cfg, F);
-    oracle_e_full(cfg, F);
+    oracle_e_full(cfg, F, step_index);
     oracle_b_half(cfg, F);
     return ORACLE_OK;
 }

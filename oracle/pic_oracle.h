@@ -20,7 +20,8 @@
  *   P  : double[6][n] per species: x,y,z (physical units, wrapped into
  *        [0,L)), ux,uy,uz (u = p/(m c) = gamma*beta, at time n-1/2).
  *   id : uint64_t[n] per species, carried along by the sort.
- * Periodic boundaries in all three axes, indices taken mod n.
+ * Periodic boundaries in all three axes, indices taken mod n (or, with
+ * bc_z == ORACLE_BC_OPEN, open z boundaries; NEXT-1).
  *
  * Parity status per function: see DESIGN.md sec. 5 (every function below is
  * pinned by a closed form, an invariant or a brute-force test in
@@ -47,7 +48,21 @@ typedef struct {
     double w[ORACLE_MAX_SPECIES];/* weight: real particles per macro-particle */
     int64_t supercell;           /* S: sort key granularity (R15) */
     int64_t sort_every;          /* K: sort at the start of step n when n % K == 0 */
+    /* z boundary (NEXT-1, reading R21): ORACLE_BC_PERIODIC,
+     * or ORACLE_BC_OPEN = first-order Mur absorbing planes k = 0 and k = nz-1
+     * for the tangential E (the incident laser enters through k = 0),
+     * field values outside [0, nz) read as zero, deposits outside dropped,
+     * particles leaving z in [0, (nz-1) dz) removed.  x and y stay periodic. */
+    int64_t bc_z;
+    /* incident plane wave (bc_z == ORACLE_BC_OPEN), travelling +z:
+     *   E_inc(z, t) = laser_e0 env(xi) sin(laser_omega xi),  xi = t + laser_t0 - z/c,
+     *   env = 0 (xi <= 0), sin^2(pi xi / (2 laser_ramp)) (xi < laser_ramp), 1 after;
+     *   (Ex, Ey) = (pol_x, pol_y) E_inc,  (Bx, By) = (-pol_y, pol_x) E_inc. */
+    double laser_e0, laser_omega, laser_ramp, laser_t0, laser_pol_x, laser_pol_y;
 } oracle_config;
+
+#define ORACLE_BC_PERIODIC 0
+#define ORACLE_BC_OPEN 1
 
 enum {
     ORACLE_OK = 0,
@@ -83,17 +98,28 @@ int64_t oracle_sort_key(const oracle_config *cfg, double x, double y, double z);
 /* a1: stable counting sort of one species by oracle_sort_key. */
 void oracle_sort(const oracle_config *cfg, int64_t n, double *P, uint64_t *id);
 
-/* a7 / O3: B -= (c dt/2) curl E ; E += c dt curl B - 4 pi dt J. */
+/* a7 / O3: B -= (c dt/2) curl E ; E += c dt curl B - 4 pi dt J.
+ * oracle_e_full advances E^n -> E^{n+1} with n = step_index (the time of the
+ * incident wave at the open boundary; unused when periodic). */
 void oracle_b_half(const oracle_config *cfg, double *F);
-void oracle_e_full(const oracle_config *cfg, double *F);
+void oracle_e_full(const oracle_config *cfg, double *F, int64_t step_index);
+
+/* NEXT-1: the incident wave amplitude E_inc(z, t) of the config (see above). */
+double oracle_laser(const oracle_config *cfg, double z, double t);
+/* NEXT-1: sets the fields to the incident wave at t = 0 (the part that
+ * entered through z = 0 before t = 0): Ex, Ey at z = k dz (k < nz),
+ * Bx, By at z = (k + 1/2) dz (k < nz - 1), every other value 0. */
+void oracle_laser_preload(const oracle_config *cfg, double *F);
 
 /* O2 step 2 for one species: gather, Boris, move, deposit, wrap, in array order.
- * J is NOT zeroed here. */
+ * J is NOT zeroed here.  With bc_z == ORACLE_BC_OPEN the particles whose new z
+ * left [0, (nz-1) dz) are removed after their deposit (the rest keep their
+ * order) and *n is updated; P keeps the [6][*n] layout (stride *n). */
 int oracle_push_species(const oracle_config *cfg, double *F, int species,
-                        int64_t n, double *P);
+                        int64_t *n, double *P, uint64_t *id);
 
-/* O2: one full time step n -> n+1 (step_index = n). */
-int oracle_step(const oracle_config *cfg, double *F, const int64_t *counts,
+/* O2: one full time step n -> n+1 (step_index = n); counts in/out. */
+int oracle_step(const oracle_config *cfg, double *F, int64_t *counts,
                 double *const *P, uint64_t *const *ids, int64_t step_index);
 
 /* Diagnostics, all on caller-owned nx*ny*nz arrays.
