@@ -14,7 +14,8 @@
  *
  * Units (R3): Gaussian, dB/dt = -c curl E, dE/dt = c curl B - 4 pi J;
  * momenta are u = p/(m c) = gamma*beta.  Positions are physical
- * coordinates in [0, L) with L = n * d per axis, periodic in x, y and z.
+ * coordinates in [0, L) with L = n * d per axis, periodic in x, y and z
+ * (or, with bc_z = PIC_BC_OPEN, open in z: z in [0, (nz-1) dz)).
  *
  * Conventions for every call:
  *  - returns PIC_OK (0) or a negative PIC_E* code; no exception, abort or
@@ -75,7 +76,27 @@ typedef struct pic_config {
                                           may leave the slab in one step (0: default 65536) */
     uint8_t nccl_id[128];              /* ncclUniqueId from rank 0 (nranks > 1) */
     void *stream;                      /* cudaStream_t all work is enqueued on */
+    /* ---- NEXT-1 (BASELINE.json configs[4]; DESIGN.md
+     * sec. 11, reading R21).  Zero-initialised fields keep the periodic box. */
+    int64_t bc_z;                      /* PIC_BC_PERIODIC, or PIC_BC_OPEN: the box ends at the
+                                          planes z = 0 and z = (nz-1) dz, where the tangential
+                                          E obeys first-order Mur (the incident laser enters
+                                          through z = 0); field values beyond them are 0,
+                                          deposits beyond them are dropped, and particles
+                                          whose z leaves [0, (nz-1) dz) are removed.  x, y
+                                          stay periodic. */
+    int64_t slab_lo, slab_hi;          /* nranks > 1: this rank's planes [slab_lo, slab_hi)
+                                          (static load balance, pic_balance_slabs); 0, 0 =
+                                          nz/nranks planes per rank */
+    double laser_e0;                   /* incident wave (PIC_BC_OPEN), travelling +z:     */
+    double laser_omega;                /*   E_inc(z,t) = e0 env(xi) sin(omega xi),         */
+    double laser_ramp;                 /*   xi = t + t0 - z/c, env = 0 for xi <= 0,       */
+    double laser_t0;                   /*   sin^2(pi xi/(2 ramp)) below ramp, then 1;      */
+    double laser_pol[2];               /*   (Ex,Ey) = pol E_inc, (Bx,By) = (-pol_y,pol_x) E_inc */
 } pic_config;
+
+#define PIC_BC_PERIODIC 0
+#define PIC_BC_OPEN 1
 
 #define PIC_FLAG_NO_GRAPH 1   /* launch kernels directly instead of CUDA graphs */
 #define PIC_FLAG_PROFILE 2    /* record per-stage CUDA events (pic_get_stage_times) */
@@ -191,7 +212,8 @@ typedef struct pic_diag {
 } pic_diag;
 
 /* Computes *out (and, if rho != NULL, copies rho^n of the local slab without
- * ghosts into the HOST array rho[nz_local][ny][nx]).  Collective when
+ * ghosts into the HOST array rho[nz_local][ny][nx]).  Periodic z only
+ * (PIC_EINVAL with PIC_BC_OPEN: the node fold assumes z images).  Collective when
  * nranks > 1 (the top node plane of a slab belongs to the slab above; the
  * Jz plane below is exchanged).  Enqueued on cfg->stream and synchronised;
  * not part of the timed step. */
@@ -200,6 +222,24 @@ int pic_diagnostics(pic_ctx *ctx, pic_diag *out, double *rho);
 /* The same for the n contexts of a PIC_FLAG_LOCAL_GROUP decomposition:
  * out[r] (and rho[r], each may be NULL) for rank r. */
 int pic_diagnostics_group(pic_ctx *const *ctxs, int n, pic_diag *out, double *const *rho);
+
+/* NEXT-1: sets E^0, B^0 of the local slab to the incident wave at t = 0
+ * (the part that entered through z = 0 before t = 0, so with laser_t0 > 0
+ * the front starts at z = c t0): Ex, Ey = pol E_inc(z, 0) at z = k dz,
+ * Bx, By = (-pol_y, pol_x) E_inc(z, 0) at z = (k + 1/2) dz below the top
+ * face, all other components 0.  Call before the first step (PIC_ESTATE
+ * otherwise); PIC_EINVAL unless bc_z == PIC_BC_OPEN.  Collective when
+ * nranks > 1 (ghost planes are exchanged at the next step). */
+int pic_laser_preload(pic_ctx *ctx);
+
+/* NEXT-1 static load balance (host only, no device): cuts the planes
+ * [0, nz) into nranks contiguous slabs z_split[r] .. z_split[r+1]
+ * (z_split[0] = 0, z_split[nranks] = nz) minimising the largest slab cost,
+ * where plane k costs plane_cost[k] (e.g. particles x t_particle + cells x
+ * t_cell); every cut is a multiple of `granule` (the supercell edge) and
+ * every slab has at least min_planes planes.  PIC_EINVAL if impossible. */
+int pic_balance_slabs(int64_t nz, int64_t nranks, int64_t granule, int64_t min_planes,
+                      const double *plane_cost, int64_t *z_split);
 
 /* Message for an error code / the last error of a context (never NULL). */
 const char *pic_strerror(int code);

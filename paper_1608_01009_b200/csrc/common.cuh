@@ -42,7 +42,14 @@ struct GridDev {
     bool periodic_z_local;   // nranks == 1: z ghosts are local images
     int nranks, rank;        // z slabs
     double zlo, zhi;         // this rank's slab [zlo, zhi) in physical z
+    // NEXT-1 open z: the box ends at z = 0 and z = zmax
+    bool open_z;             // PIC_BC_OPEN (x, y stay periodic)
+    bool open_lo, open_hi;   // this rank holds the global z = 0 / z = zmax face
+    double zmax;             // open: particles live in [0, zmax), zmax = (nz_global - 1) dz
+    double mur_a;            // (c dt - dz) / (c dt + dz)
+    const double *laser;     // open_lo: incident values of this step [Ex, Ey][I0', I1, I1', I0]
 };
+
 
 __host__ __device__ inline int64_t pidx(const GridDev &g, int i, int j, int k)
 {

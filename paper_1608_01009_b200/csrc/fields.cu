@@ -10,7 +10,8 @@
 // index wraps.  The producing thread also stores its value into every
 // periodic ghost image (x, y always; z when the slab is the whole box), so
 // no separate ghost-fill pass runs (HBM-bound; the ghost stores are a
-// surface term).
+// surface term).  With open z (NEXT-1) the faces z = 0 and z = zmax take
+// first-order Mur with the incident laser (k_e_full, k_laser_coeffs).
 #include "kernels.cuh"
 
 namespace pic {
@@ -32,9 +33,14 @@ __global__ void __launch_bounds__(256) k_b_half(GridDev g, double *__restrict__ 
     const double bx = fma(-coef, cx, Bx[o]);
     const double by = fma(-coef, cy, By[o]);
     const double bz = fma(-coef, cz, Bz[o]);
+    // open z (NEXT-1): Bx, By of the top plane sit at z = zmax + dz/2, outside
+    // the box; they are not advanced
+    const bool outside = g.open_hi && k == g.nz - 1;
     for_images(g, i, j, k, [&](int64_t p) {
-        Bx[p] = bx;
-        By[p] = by;
+        if (!outside) {
+            Bx[p] = bx;
+            By[p] = by;
+        }
         Bz[p] = bz;
     });
 }
@@ -68,13 +74,118 @@ k_e_full(GridDev g, double *__restrict__ EB, double *__restrict__ Jc, double *__
     const double cx = (bz - Bz[o - sy]) * g.inv_dy - (by - By[o - sz]) * g.inv_dz;
     const double cy = (bx - Bx[o - sz]) * g.inv_dz - (bz - Bz[o - 1]) * g.inv_dx;
     const double cz = (by - By[o - 1]) * g.inv_dx - (bx - Bx[o - sy]) * g.inv_dy;
-    const double ex = fma(-coefJ, jx, fma(coefE, cx, Ex[o]));
-    const double ey = fma(-coefJ, jy, fma(coefE, cy, Ey[o]));
+    const double ex_old = Ex[o], ey_old = Ey[o];
+    const double ex = fma(-coefJ, jx, fma(coefE, cx, ex_old));
+    const double ey = fma(-coefJ, jy, fma(coefE, cy, ey_old));
     const double ez = fma(-coefJ, jz, fma(coefE, cz, Ez[o]));
+    if (!g.open_z) {
+        for_images(g, i, j, k, [&](int64_t p) {
+            Ex[p] = ex;
+            Ey[p] = ey;
+            Ez[p] = ez;
+        });
+        return;
+    }
+    // ---- open z (NEXT-1, reading R21) ----
+    // the tangential E of the faces z = 0 (local plane 0 of the lowest rank)
+    // and z = zmax (local plane nz-1 of the highest) come from first-order Mur
+    // on the scattered field E - E_inc, evaluated by the thread of the plane
+    // next to the face, which holds that plane's old and new value; Ez of the
+    // top plane lies outside the box and is not advanced
+    const bool face_lo = g.open_lo && k == 0, face_hi = g.open_hi && k == g.nz - 1;
     for_images(g, i, j, k, [&](int64_t p) {
-        Ex[p] = ex;
-        Ey[p] = ey;
-        Ez[p] = ez;
+        if (!face_lo && !face_hi) {
+            Ex[p] = ex;
+            Ey[p] = ey;
+        }
+        if (!face_hi) Ez[p] = ez;
+    });
+    const double a = g.mur_a;
+    if (g.open_lo && k == 1) {
+        // E0' = I0' + (E1 - I1) + a ((E1' - I1') - (E0 - I0)); laser = [c][I0', I1, I1', I0]
+        const double *I = g.laser;
+        const double e0x = Ex[o - sz], e0y = Ey[o - sz];
+        const double nx0 = I[0] + (ex_old - I[1]) + a * ((ex - I[2]) - (e0x - I[3]));
+        const double ny0 = I[4] + (ey_old - I[5]) + a * ((ey - I[6]) - (e0y - I[7]));
+        for_images(g, i, j, 0, [&](int64_t p) {
+            Ex[p] = nx0;
+            Ey[p] = ny0;
+        });
+    }
+    if (g.open_hi && k == g.nz - 2) {
+        // EK' = E(K-1) + a (E(K-1)' - EK)
+        const double eKx = Ex[o + sz], eKy = Ey[o + sz];
+        const double nxK = ex_old + a * (ex - eKx);
+        const double nyK = ey_old + a * (ey - eKy);
+        for_images(g, i, j, g.nz - 1, [&](int64_t p) {
+            Ex[p] = nxK;
+            Ey[p] = nyK;
+        });
+    }
+    if (g.nranks == 1) {
+        // no z images and no slab exchange: clear the z ghost planes of J_next
+        // (the deposit spills beyond the faces; those values are dropped)
+        const int kz0 = k == 0 ? -kGhost : (k == g.nz - 1 ? g.nz : 0);
+        if (k == 0 || k == g.nz - 1)
+            for (int kk = kz0; kk < kz0 + kGhost; ++kk)
+                for_images(g, i, j, kk, [&](int64_t p) {
+                    Jn[p] = 0.0;
+                    Jn[cs + p] = 0.0;
+                    Jn[2 * cs + p] = 0.0;
+                });
+    }
+}
+
+// NEXT-1: the incident values of step n -> n+1 at the open face z = 0, from
+// the device step counter (so the step stays one CUDA graph):
+// laser[c*4 + {0,1,2,3}] = pol_c {E_inc(0,t'), E_inc(dz,t), E_inc(dz,t'), E_inc(0,t)},
+// t = n dt, t' = (n+1) dt;  E_inc(z,t) = e0 env(xi) sin(omega xi), xi = t + t0 - z/c.
+struct LaserDev {
+    double e0, omega, ramp, t0, pol[2];
+};
+
+__device__ double laser_inc(const LaserDev &L, double c, double z, double t)
+{
+    const double xi = t + L.t0 - z / c;
+    if (!(xi > 0.0)) return 0.0;
+    double env = 1.0;
+    if (xi < L.ramp) {
+        const double sr = sin(M_PI * xi / (2.0 * L.ramp));
+        env = sr * sr;
+    }
+    return L.e0 * env * sin(L.omega * xi);
+}
+
+__global__ void k_laser_coeffs(GridDev g, LaserDev L, int64_t *step, double *laser)
+{
+    if (threadIdx.x != 0) return;
+    const int64_t n = *step;
+    const double t0 = (double)n * g.dt, t1 = (double)(n + 1) * g.dt;
+    const double v[4] = {laser_inc(L, g.c, 0.0, t1), laser_inc(L, g.c, g.dz, t0), laser_inc(L, g.c, g.dz, t1),
+                         laser_inc(L, g.c, 0.0, t0)};
+    for (int c = 0; c < 2; ++c)
+        for (int q = 0; q < 4; ++q) laser[4 * c + q] = L.pol[c] * v[q];
+    *step = n + 1;
+}
+
+// NEXT-1: fields of the local slab = the incident wave at t = 0 (pic_laser_preload)
+__global__ void __launch_bounds__(256) k_laser_preload(GridDev g, LaserDev L, double *__restrict__ EB)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= g.nx || j >= g.ny) return;
+    const int64_t cs = g.cs;
+    const int kg = g.k0 + k;
+    const double e = laser_inc(L, g.c, (double)kg * g.dz, 0.0);
+    const double b = kg < g.nz_global - 1 ? laser_inc(L, g.c, ((double)kg + 0.5) * g.dz, 0.0) : 0.0;
+    for_images(g, i, j, k, [&](int64_t p) {
+        EB[p] = L.pol[0] * e;
+        EB[cs + p] = L.pol[1] * e;
+        EB[2 * cs + p] = 0.0;
+        EB[3 * cs + p] = -L.pol[1] * b;
+        EB[4 * cs + p] = L.pol[0] * b;
+        EB[5 * cs + p] = 0.0;
     });
 }
 
@@ -112,6 +223,19 @@ void launch_e_full(const GridDev &g, double *EB, double *Jcur, double *Jnext, cu
     const dim3 bs(32, 8, 1);
     k_e_full<<<field_grid(g, bs), bs, 0, st>>>(g, EB, Jcur, Jnext, g.c * g.dt,
                                                 4.0 * M_PI * g.dt);
+}
+
+void launch_laser_coeffs(const GridDev &g, const double laser[6], int64_t *step, double *out, cudaStream_t st)
+{
+    const LaserDev L{laser[0], laser[1], laser[2], laser[3], {laser[4], laser[5]}};
+    k_laser_coeffs<<<1, 32, 0, st>>>(g, L, step, out);
+}
+
+void launch_laser_preload(const GridDev &g, const double laser[6], double *EB, cudaStream_t st)
+{
+    const LaserDev L{laser[0], laser[1], laser[2], laser[3], {laser[4], laser[5]}};
+    const dim3 bs(32, 8, 1);
+    k_laser_preload<<<field_grid(g, bs), bs, 0, st>>>(g, L, EB);
 }
 
 void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st)

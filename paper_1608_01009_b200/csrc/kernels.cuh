@@ -17,6 +17,12 @@ void launch_b_half(const GridDev &g, double *EB, cudaStream_t st, int kbegin = 0
 void launch_e_full(const GridDev &g, double *EB, double *Jcur, double *Jnext, cudaStream_t st);
 // Copies interior values of `ncomp` components to their ghost images.
 void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st);
+// NEXT-1 (open z): laser = {e0, omega, ramp, t0, pol_x, pol_y}.  Writes the
+// incident values of step *step at z = 0 into out[8] (g.laser) and
+// increments *step; a one-thread kernel inside the step's graph.
+void launch_laser_coeffs(const GridDev &g, const double laser[6], int64_t *step, double *out, cudaStream_t st);
+// E^0, B^0 of the local slab = the incident wave at t = 0 (pic_laser_preload)
+void launch_laser_preload(const GridDev &g, const double laser[6], double *EB, cudaStream_t st);
 
 // ---- push_naive.cu ----
 void launch_push_naive(const GridDev &g, const double *EB, double *J, const ParticlesDev &in,

@@ -108,6 +108,13 @@ __device__ __forceinline__ double wrap_coord(double x, double L)
     return (x >= L) ? x - L : ((x < 0.0) ? wl : x);
 }
 
+// z after a move: periodic wrap (R7), or unchanged in an open box (NEXT-1;
+// a particle that left [0, zmax) is removed by store_particle)
+__device__ __forceinline__ double wrap_z(const GridDev &g, double z)
+{
+    return g.open_z ? z : wrap_coord(z, g.Lz);
+}
+
 // Villasenor-Buneman deposit of one straight in-cell segment
 // (PAPER.md:48).  P1, P2 are local coordinates inside the
 // segment's cell (components in [0,1] up to rounding); add(comp, di, dj, dk,

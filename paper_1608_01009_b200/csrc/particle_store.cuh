@@ -13,13 +13,21 @@ __device__ __forceinline__ bool store_particle(const GridDev &g, const SpeciesDe
                                                int64_t p, double x, double y, double z, double ux,
                                                double uy, double uz, bool copy_id, unsigned *err)
 {
+    if (g.open_z && !(z >= 0.0 && z < g.zmax)) {
+        // NEXT-1: left the open box through z = 0 or z = zmax (its current up to
+        // the face is deposited): absorbed, the slot is dead until the next sort
+        out.x[p] = kDeadX;
+        return true;
+    }
     if (g.nranks > 1 && !(z >= g.zlo && z < g.zhi)) {
-        // new owner from the wrapped z; one step moves < 1 cell, so it is the lower
-        // (dir 0) or the upper (dir 1) neighbour in the periodic ring of slabs
-        int owner = (int)floor(z / (g.zhi - g.zlo));
-        owner = owner < 0 ? 0 : (owner >= g.nranks ? g.nranks - 1 : owner);
-        const int dir = (owner == (g.rank + g.nranks - 1) % g.nranks) ? 0 : 1;
-        if (dir == 1 && owner != (g.rank + 1) % g.nranks) atomicOr(err, kErrDisplacement);
+        // one step moves < 1 cell, so the new owner is the lower (dir 0) or the
+        // upper (dir 1) neighbour in the ring of slabs: the nearer face, measured
+        // periodically (slabs may differ in width, pic_balance_slabs)
+        double ddn = g.zlo - z, dup = z - g.zhi;
+        if (ddn < 0.0) ddn += g.Lz;
+        if (dup < 0.0) dup += g.Lz;
+        const int dir = ddn <= dup ? 0 : 1;
+        if (fmin(ddn, dup) > g.dz) atomicOr(err, kErrDisplacement);
         const unsigned slot = atomicAdd(sp.mig.count + dir, 1u);
         if (slot < (unsigned)sp.mig.cap) {
             double *b = sp.mig.send[dir] + 1;

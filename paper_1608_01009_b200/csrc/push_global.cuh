@@ -68,7 +68,7 @@ __device__ __forceinline__ void push_one_global(const GridDev &g, const double *
     }
     x = wrap_coord(xn, g.Lx);
     y = wrap_coord(yn, g.Ly);
-    z = wrap_coord(zn, g.Lz);
+    z = wrap_z(g, zn);
 }
 
 }  // namespace pic

@@ -305,7 +305,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
             if (ok)
                 store_particle(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
-                               wrap_coord(zn, g.Lz), ux, uy, uz, copy_id != 0, err);
+                               wrap_z(g, zn), ux, uy, uz, copy_id != 0, err);
             else
                 store_particle(g, sp, out, in.id, p, x, y, z, ux, uy, uz, copy_id != 0, err);
             if (ok) {

@@ -54,6 +54,7 @@ struct Layout {
     size_t off_msend[PIC_MAX_SPECIES][2] = {}, off_mrecv[PIC_MAX_SPECIES][2] = {}, off_mcnt = 0;
     size_t off_jrecv[2] = {};
     size_t off_rho = 0, off_rho_prev = 0, off_gauss0 = 0, off_acc = 0;   // diagnostics
+    size_t off_laser = 0, off_step = 0;                                  // NEXT-1 open z
     size_t total = 0;
 };
 
@@ -73,11 +74,25 @@ std::string validate(const pic_config *c)
         if (!std::isfinite(c->q[s]) || !std::isfinite(c->w[s])) return "non-finite q or w";
     }
     if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return "bad rank / nranks";
-    if (c->nz % c->nranks) return "nz must be divisible by nranks";
     if (c->supercell < 1) return "supercell must be >= 1";
-    const int64_t nzl = c->nz / c->nranks;
+    if (c->bc_z != PIC_BC_PERIODIC && c->bc_z != PIC_BC_OPEN) return "bc_z must be PIC_BC_PERIODIC or PIC_BC_OPEN";
+    if (c->bc_z == PIC_BC_OPEN && c->nz < 3) return "an open z box needs nz >= 3";
+    if (c->bc_z == PIC_BC_OPEN &&
+        !(std::isfinite(c->laser_e0) && std::isfinite(c->laser_omega) && c->laser_ramp >= 0.0 &&
+          std::isfinite(c->laser_ramp) && std::isfinite(c->laser_t0) && std::isfinite(c->laser_pol[0]) &&
+          std::isfinite(c->laser_pol[1])))
+        return "bad laser parameters";
+    const bool explicit_slab = c->nranks > 1 && (c->slab_lo != 0 || c->slab_hi != 0);
+    if (explicit_slab) {
+        if (!(c->slab_lo >= 0 && c->slab_lo < c->slab_hi && c->slab_hi <= c->nz)) return "bad slab_lo / slab_hi";
+        if ((c->rank == 0) != (c->slab_lo == 0) || (c->rank == c->nranks - 1) != (c->slab_hi == c->nz))
+            return "slab_lo / slab_hi: rank 0 starts at 0, the last rank ends at nz";
+    } else if (c->nz % c->nranks) {
+        return "nz must be divisible by nranks (or set slab_lo / slab_hi)";
+    }
+    const int64_t nzl = explicit_slab ? c->slab_hi - c->slab_lo : c->nz / c->nranks;
     if (c->nx % c->supercell || c->ny % c->supercell || nzl % c->supercell)
-        return "supercell must divide nx, ny and nz/nranks";
+        return "supercell must divide nx, ny and the slab thickness";
     if (c->nranks > 1 && nzl < 4) return "z slabs must be at least 4 cells thick";
     if (c->sort_every < 0) return "sort_every must be >= 0";
     if (c->migrate_capacity < 0 || c->migrate_capacity >= (int64_t(1) << 28)) return "bad migrate_capacity";
@@ -91,9 +106,10 @@ Layout make_layout(const pic_config *c)
     GridDev &g = L.g;
     g.nx = (int)c->nx;
     g.ny = (int)c->ny;
-    g.nz = (int)(c->nz / c->nranks);
+    const bool explicit_slab = c->nranks > 1 && (c->slab_lo != 0 || c->slab_hi != 0);
+    g.nz = (int)(explicit_slab ? c->slab_hi - c->slab_lo : c->nz / c->nranks);
     g.nz_global = (int)c->nz;
-    g.k0 = (int)(c->rank * g.nz);
+    g.k0 = (int)(explicit_slab ? c->slab_lo : c->rank * g.nz);
     g.X = g.nx + 2 * kGhost;
     g.X += g.X & 1;   // 16-byte row pitch (TMA global strides)
     g.Y = g.ny + 2 * kGhost;
@@ -106,11 +122,17 @@ Layout make_layout(const pic_config *c)
     g.Lx = c->nx * c->dx; g.Ly = c->ny * c->dy; g.Lz = c->nz * c->dz;
     g.S = (int)c->supercell;
     g.nsx = g.nx / g.S; g.nsy = g.ny / g.S; g.nsz = g.nz / g.S;
-    g.periodic_z_local = (c->nranks == 1);
+    g.open_z = c->bc_z == PIC_BC_OPEN;
+    g.periodic_z_local = (c->nranks == 1) && !g.open_z;
     g.nranks = (int)c->nranks;
     g.rank = (int)c->rank;
     g.zlo = c->nranks == 1 ? 0.0 : (double)g.k0 * c->dz;
     g.zhi = c->nranks == 1 ? g.Lz : (c->rank == c->nranks - 1 ? g.Lz : (double)(g.k0 + g.nz) * c->dz);
+    g.open_lo = g.open_z && c->rank == 0;
+    g.open_hi = g.open_z && c->rank == c->nranks - 1;
+    g.zmax = g.open_z ? (double)(c->nz - 1) * c->dz : g.Lz;
+    g.mur_a = (c->c * c->dt - c->dz) / (c->c * c->dt + c->dz);
+    g.laser = nullptr;   // set by pic_init
     L.ncells = (int64_t)g.nx * g.ny * g.nz;
     L.n_sc = (int64_t)g.nsx * g.nsy * g.nsz;
     L.mig = c->nranks > 1 ? (c->migrate_capacity ? c->migrate_capacity : kDefaultMigrate) : 0;
@@ -154,6 +176,8 @@ Layout make_layout(const pic_config *c)
     L.off_rho_prev = o; o = align_up(o + sizeof(double) * (size_t)g.cs);
     L.off_gauss0 = o; o = align_up(o + sizeof(double) * (size_t)g.cs);
     L.off_acc = o; o = align_up(o + sizeof(double) * kAccSlots);
+    L.off_laser = o; o = align_up(o + sizeof(double) * 8);
+    L.off_step = o; o = align_up(o + sizeof(int64_t));
     L.total = o;
     return L;
 }
@@ -264,6 +288,10 @@ struct pic_ctx {
     double *jrecv[2] = {nullptr, nullptr};     // [from rank-1, from rank+1]
     // diagnostics (diag.cu): padded node arrays and accumulators
     double *rho = nullptr, *rho_prev = nullptr, *gauss0 = nullptr, *acc = nullptr;
+    // NEXT-1 open z: incident values of the current step and the device step counter
+    double *laser = nullptr;
+    int64_t *dev_step = nullptr;
+    double laser_par[6] = {0, 0, 0, 0, 0, 0};   // e0, omega, ramp, t0, pol_x, pol_y
     int64_t diag_last_step = -2;
     bool diag_have_g0 = false;
     int64_t step_index = 0;
@@ -388,19 +416,31 @@ std::vector<Msg> msgs_current(pic_ctx *ctx, int jcur)
     return m;
 }
 
+// the ring of slabs is cut at an open z box's faces (NEXT-1): rank 0 has no
+// lower and the last rank no upper neighbour
+bool has_neighbour(const pic_config &c, int rank, int dir)
+{
+    if (c.bc_z != PIC_BC_OPEN) return true;
+    return dir == 0 ? rank > 0 : rank < c.nranks - 1;
+}
+
 int exchange_nccl(pic_ctx *ctx, const std::vector<Msg> &msgs)
 {
     NcclApi *api = nccl_api();
     if (!api || !ctx->comm) return fail(ctx, PIC_ENCCL, "NCCL not initialised");
     const int r = (int)ctx->cfg.rank, n = (int)ctx->cfg.nranks;
     const int dn = (r + n - 1) % n, up = (r + 1) % n;
+    const bool has_dn = has_neighbour(ctx->cfg, r, 0), has_up = has_neighbour(ctx->cfg, r, 1);
     ncclResult_t e = api->groupStart();
     // sends and receives are each posted in message order, so with two ranks
-    // (dn == up) the i-th send matches the peer's i-th receive
+    // (dn == up) the i-th send matches the peer's i-th receive; a message of
+    // direction d goes to the neighbour on side d and arrives from the other side
     for (const Msg &m : msgs)
-        if (e == ncclSuccess) e = api->send(m.send, m.count, ncclFloat64, m.dir == 0 ? dn : up, ctx->comm, ctx->st);
+        if (e == ncclSuccess && (m.dir == 0 ? has_dn : has_up))
+            e = api->send(m.send, m.count, ncclFloat64, m.dir == 0 ? dn : up, ctx->comm, ctx->st);
     for (const Msg &m : msgs)
-        if (e == ncclSuccess) e = api->recv(m.recv, m.count, ncclFloat64, m.dir == 0 ? up : dn, ctx->comm, ctx->st);
+        if (e == ncclSuccess && (m.dir == 0 ? has_up : has_dn))
+            e = api->recv(m.recv, m.count, ncclFloat64, m.dir == 0 ? up : dn, ctx->comm, ctx->st);
     const ncclResult_t e2 = api->groupEnd();
     if (e != ncclSuccess || e2 != ncclSuccess)
         return fail(ctx, PIC_ENCCL, std::string("NCCL exchange: ") +
@@ -414,6 +454,7 @@ int exchange_local(pic_ctx *const *ctxs, int n, const std::vector<std::vector<Ms
     for (int r = 0; r < n; ++r) {
         for (size_t i = 0; i < msgs[r].size(); ++i) {
             const Msg &m = msgs[r][i];
+            if (!has_neighbour(ctxs[r]->cfg, r, m.dir == 0 ? 1 : 0)) continue;   // open face
             const int src = m.dir == 0 ? (r + 1) % n : (r + n - 1) % n;   // who sends toward r
             PIC_CUDA(ctxs[r], cudaMemcpyAsync(m.recv, msgs[src][i].send, m.count * sizeof(double),
                                               cudaMemcpyDeviceToDevice, ctxs[r]->st));
@@ -479,7 +520,13 @@ int phase_fields_e(pic_ctx *ctx, int jcur, bool profile)
             launches += 2;
         }
     }
-    launch_b_half(g, ctx->EB, ctx->st, ctx->slabs ? -1 : 0);
+    // slabs compute the lower ghost plane of B^{n+1/2} locally, except below an
+    // open face (it lies outside the box and stays 0)
+    launch_b_half(g, ctx->EB, ctx->st, ctx->slabs && !g.open_lo ? -1 : 0);
+    if (g.open_lo) {
+        launch_laser_coeffs(g, ctx->laser_par, ctx->dev_step, ctx->laser, ctx->st);
+        ++launches;
+    }
     launch_e_full(g, ctx->EB, ctx->J[jcur], ctx->J[1 - jcur], ctx->st);
     return launches + 2;
 }
@@ -732,6 +779,15 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->rho_prev = (double *)(ctx->ws + L.off_rho_prev);
     ctx->gauss0 = (double *)(ctx->ws + L.off_gauss0);
     ctx->acc = (double *)(ctx->ws + L.off_acc);
+    ctx->laser = (double *)(ctx->ws + L.off_laser);
+    ctx->dev_step = (int64_t *)(ctx->ws + L.off_step);
+    ctx->L.g.laser = ctx->laser;
+    ctx->laser_par[0] = cfg->laser_e0;
+    ctx->laser_par[1] = cfg->laser_omega;
+    ctx->laser_par[2] = cfg->laser_ramp;
+    ctx->laser_par[3] = cfg->laser_t0;
+    ctx->laser_par[4] = cfg->laser_pol[0];
+    ctx->laser_par[5] = cfg->laser_pol[1];
     ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell);
     configure_tile_kernels();
     {
@@ -749,6 +805,12 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     for (int s = 0; e == cudaSuccess && s < cfg->n_species; ++s)
         e = cudaMemsetAsync(ctx->sc_off[s], 0, sizeof(int64_t) * (size_t)(L.n_sc + 1), ctx->st);
     if (e == cudaSuccess) e = cudaMemsetAsync(ctx->ws + L.off_err, 0, L.total - L.off_err, ctx->st);
+    // receive buffers: a face of an open box never receives, so they must read 0
+    for (int s = 0; e == cudaSuccess && s < cfg->n_species; ++s)
+        for (int d = 0; e == cudaSuccess && d < 2; ++d)
+            if (ctx->mrecv[s][d]) e = cudaMemsetAsync(ctx->mrecv[s][d], 0, sizeof(double) * (1 + 7 * (size_t)L.mig), ctx->st);
+    for (int d = 0; e == cudaSuccess && d < 2; ++d)
+        if (ctx->jrecv[d]) e = cudaMemsetAsync(ctx->jrecv[d], 0, sizeof(double) * 3 * 2 * (size_t)L.g.X * L.g.Y, ctx->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
     if (e != cudaSuccess) {
         delete ctx;
@@ -777,8 +839,9 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
         return fail(ctx, PIC_EINVAL, "bad particle arrays");
     const GridDev &g = ctx->L.g;
     for (int64_t p = 0; p < n; ++p) {
-        if (!(x[p] >= 0.0 && x[p] < g.Lx && y[p] >= 0.0 && y[p] < g.Ly && z[p] >= 0.0 && z[p] < g.Lz))
-            return fail(ctx, PIC_EINVAL, "particle position outside [0, L)");
+        if (!(x[p] >= 0.0 && x[p] < g.Lx && y[p] >= 0.0 && y[p] < g.Ly && z[p] >= 0.0 && z[p] < g.zmax))
+            return fail(ctx, PIC_EINVAL, g.open_z ? "particle position outside [0, Lx) x [0, Ly) x [0, (nz-1) dz)"
+                                                  : "particle position outside [0, L)");
     }
     const double *src[6] = {x, y, z, ux, uy, uz};
     std::vector<double> sel[6];
@@ -874,7 +937,7 @@ int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout, double *x, do
     const double *src[6] = {A.x, A.y, A.z, A.ux, A.uy, A.uz};
     double *dst[6] = {x, y, z, ux, uy, uz};
     const int64_t capacity = *n_inout;
-    if (!ctx->slabs) {   // every slot is live
+    if (!ctx->slabs && !ctx->L.g.open_z) {   // every slot is live
         *n_inout = slots;
         if (capacity < slots) return fail(ctx, PIC_ECAPACITY, "output arrays too small");
         for (int c = 0; c < 6 && slots > 0; ++c)
@@ -886,7 +949,7 @@ int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout, double *x, do
         PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         return PIC_OK;
     }
-    // slabs: skip dead slots (x == -1) left by migration
+    // slabs / open z: skip dead slots (x == -1) left by migration or absorption
     std::vector<double> buf[6];
     std::vector<uint64_t> ibuf((size_t)slots);
     for (int c = 0; c < 6; ++c) {
@@ -916,7 +979,7 @@ int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout, double *x, do
 int pic_get_count(pic_ctx *ctx, int species, int64_t *n)
 {
     if (!ctx || !n || species < 0 || species >= ctx->cfg.n_species) return PIC_EINVAL;
-    if (!ctx->slabs) return device_slots(ctx, species, n);
+    if (!ctx->slabs && !ctx->L.g.open_z) return device_slots(ctx, species, n);
     int64_t cap = 0;
     int rc = pic_get_particles(ctx, species, &cap, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     if (rc != PIC_OK && rc != PIC_ECAPACITY) return rc;
@@ -1024,6 +1087,7 @@ int pic_diagnostics(pic_ctx *ctx, pic_diag *out, double *rho)
 {
     if (!ctx) return PIC_EINVAL;
     if (ctx->local_group) return fail(ctx, PIC_ESTATE, "PIC_FLAG_LOCAL_GROUP contexts use pic_diagnostics_group");
+    if (ctx->L.g.open_z) return fail(ctx, PIC_EINVAL, "diagnostics assume a periodic z box");
     if (ctx->ghosts_stale) {
         int rc = exchange_nccl(ctx, msgs_fields(ctx, 0, 6));
         if (rc != PIC_OK) return rc;
@@ -1042,6 +1106,7 @@ int pic_diagnostics_group(pic_ctx *const *ctxs, int n, pic_diag *out, double *co
         if (!ctxs[r] || !ctxs[r]->local_group || ctxs[r]->cfg.nranks != n || ctxs[r]->cfg.rank != r)
             return fail(ctxs[r], PIC_EINVAL, "pic_diagnostics_group needs PIC_FLAG_LOCAL_GROUP ranks 0..n-1");
     }
+    if (ctxs[0]->L.g.open_z) return fail(ctxs[0], PIC_EINVAL, "diagnostics assume a periodic z box");
     auto all = [&](auto f) {
         std::vector<std::vector<Msg>> m(n);
         for (int r = 0; r < n; ++r) m[r] = f(ctxs[r]);
@@ -1062,6 +1127,67 @@ int pic_diagnostics_group(pic_ctx *const *ctxs, int n, pic_diag *out, double *co
         rc = diag_nodes(ctxs[r], out ? out + r : nullptr, rho ? rho[r] : nullptr);
         if (rc != PIC_OK) return rc;
     }
+    return PIC_OK;
+}
+
+int pic_laser_preload(pic_ctx *ctx)
+{
+    if (!ctx) return PIC_EINVAL;
+    if (!ctx->L.g.open_z) return fail(ctx, PIC_EINVAL, "pic_laser_preload needs bc_z == PIC_BC_OPEN");
+    if (ctx->step_index != 0) return fail(ctx, PIC_ESTATE, "pic_laser_preload before the first step");
+    launch_laser_preload(ctx->L.g, ctx->laser_par, ctx->EB, ctx->st);
+    ctx->launches += 1;
+    ctx->ghosts_stale = ctx->slabs;   // z ghost planes come from the neighbours
+    PIC_CUDA(ctx, cudaGetLastError());
+    PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return PIC_OK;
+}
+
+int pic_balance_slabs(int64_t nz, int64_t nranks, int64_t granule, int64_t min_planes,
+                      const double *plane_cost, int64_t *z_split)
+{
+    if (nz < 1 || nranks < 1 || granule < 1 || min_planes < 1 || !plane_cost || !z_split) return PIC_EINVAL;
+    if (nz % granule) return PIC_EINVAL;
+    const int64_t ng = nz / granule;                           // granules
+    const int64_t mg = (min_planes + granule - 1) / granule;   // min granules per slab
+    if (ng < nranks * mg) return PIC_EINVAL;
+    std::vector<double> pre((size_t)ng + 1, 0.0);              // prefix cost over granules
+    for (int64_t q = 0; q < ng; ++q) {
+        double c = 0.0;
+        for (int64_t k = q * granule; k < (q + 1) * granule; ++k) {
+            if (!(plane_cost[k] >= 0.0) || !std::isfinite(plane_cost[k])) return PIC_EINVAL;
+            c += plane_cost[k];
+        }
+        pre[(size_t)q + 1] = pre[(size_t)q] + c;
+    }
+    // Is a largest slab cost <= T possible?  Greedy from z = 0: every slab
+    // takes as many granules as fit under T, at least mg, and leaves mg for
+    // each slab after it (taking more never hurts the slabs after it).
+    auto feasible = [&](double T, std::vector<int64_t> *out) {
+        int64_t q = 0;
+        if (out) out->assign(1, 0);
+        for (int64_t r = 0; r < nranks; ++r) {
+            const int64_t lo = q + mg, hi = ng - (nranks - 1 - r) * mg;
+            if (lo > hi) return false;
+            int64_t e = lo;
+            if (r == nranks - 1)
+                e = ng;
+            else
+                while (e < hi && pre[(size_t)e + 1] - pre[(size_t)q] <= T) ++e;
+            if (pre[(size_t)e] - pre[(size_t)q] > T) return false;
+            if (out) out->push_back(e);
+            q = e;
+        }
+        return true;
+    };
+    double lo = 0.0, hi = pre[(size_t)ng];   // hi is always feasible
+    for (int it = 0; it < 200 && hi - lo > 1e-13 * hi; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (feasible(mid, nullptr)) hi = mid; else lo = mid;
+    }
+    std::vector<int64_t> g;
+    feasible(hi, &g);
+    for (int64_t r = 0; r <= nranks; ++r) z_split[r] = g[(size_t)r] * granule;
     return PIC_OK;
 }
 

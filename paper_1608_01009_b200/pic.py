@@ -32,7 +32,7 @@ EXPORTS = [
     "pic_get_fields", "pic_get_particles", "pic_get_count", "pic_get_step_index",
     "pic_get_stage_times", "pic_get_launch_count", "pic_strerror", "pic_last_error",
     "pic_destroy", "pic_nccl_unique_id", "pic_step_group", "pic_diagnostics",
-    "pic_diagnostics_group",
+    "pic_diagnostics_group", "pic_laser_preload", "pic_balance_slabs",
 ]
 
 
@@ -53,7 +53,15 @@ class PicConfig(C.Structure):
         ("migrate_capacity", C.c_int64),
         ("nccl_id", C.c_uint8 * 128),
         ("stream", C.c_void_p),
+        ("bc_z", C.c_int64),
+        ("slab_lo", C.c_int64), ("slab_hi", C.c_int64),
+        ("laser_e0", C.c_double), ("laser_omega", C.c_double), ("laser_ramp", C.c_double),
+        ("laser_t0", C.c_double), ("laser_pol", C.c_double * 2),
     ]
+
+
+BC_PERIODIC = 0
+BC_OPEN = 1
 
 
 class PicDiag(C.Structure):
@@ -118,6 +126,8 @@ def lib():
         L.pic_diagnostics.argtypes = [C.c_void_p, C.POINTER(PicDiag), dp]
         L.pic_diagnostics_group.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(PicDiag),
                                             C.POINTER(dp)]
+        L.pic_laser_preload.argtypes = [C.c_void_p]
+        L.pic_balance_slabs.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, dp, i64p]
         for name in EXPORTS:
             if name not in ("pic_strerror", "pic_last_error", "pic_destroy"):
                 getattr(L, name).restype = C.c_int
@@ -131,8 +141,9 @@ def _dptr(a):
 
 def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity=None,
                 supercell=4, sort_every=20, rank=0, nranks=1, flags=0, nccl_id=None,
-                migrate_capacity=0):
-    """species: list of (q, m, w)."""
+                migrate_capacity=0, bc_z=BC_PERIODIC, slab=None, laser=None):
+    """species: list of (q, m, w); slab: (lo, hi) planes of this rank;
+    laser: dict e0, omega, ramp, t0, pol (open z, NEXT-1)."""
     cfg = PicConfig()
     cfg.nx, cfg.ny, cfg.nz = nx, ny, nz
     cfg.dx, cfg.dy, cfg.dz = dx, dy, dz
@@ -146,7 +157,25 @@ def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity
     cfg.migrate_capacity = migrate_capacity
     if nccl_id is not None:
         C.memmove(cfg.nccl_id, bytes(nccl_id), 128)
+    cfg.bc_z = bc_z
+    if slab is not None and nranks > 1:
+        cfg.slab_lo, cfg.slab_hi = int(slab[0]), int(slab[1])
+    if laser:
+        cfg.laser_e0, cfg.laser_omega = laser["e0"], laser["omega"]
+        cfg.laser_ramp, cfg.laser_t0 = laser["ramp"], laser["t0"]
+        cfg.laser_pol[0], cfg.laser_pol[1] = laser["pol"]
     return cfg
+
+
+def balance_slabs(nz, nranks, granule, min_planes, plane_cost):
+    """pic_balance_slabs: z cut planes [0, ..., nz] minimising the largest slab cost."""
+    cost = np.ascontiguousarray(plane_cost, dtype=np.float64)
+    assert cost.size == nz
+    out = (C.c_int64 * (nranks + 1))()
+    rc = lib().pic_balance_slabs(nz, nranks, granule, min_planes, _dptr(cost), out)
+    if rc != PIC_OK:
+        raise PicError(rc, "pic_balance_slabs")
+    return list(out)
 
 
 class Simulation:
@@ -175,7 +204,9 @@ class Simulation:
         with torch.cuda.device(self.device):
             self._check(L.pic_init(C.byref(cfg), C.c_void_p(aligned), nbytes.value, C.byref(self.ctx)),
                         None)
-        self.nx, self.ny, self.nz_local = cfg.nx, cfg.ny, cfg.nz // cfg.nranks
+        self.nx, self.ny = cfg.nx, cfg.ny
+        self.nz_local = (cfg.slab_hi - cfg.slab_lo if cfg.nranks > 1 and (cfg.slab_lo or cfg.slab_hi)
+                         else cfg.nz // cfg.nranks)
         self.n_species = cfg.n_species
 
     def _check(self, rc, ctx="self"):
@@ -201,6 +232,10 @@ class Simulation:
 
     def step(self, n=1):
         self._check(lib().pic_step(self.ctx, int(n)))
+
+    def laser_preload(self):
+        """pic_laser_preload: E^0, B^0 = the incident wave at t = 0 (open z)."""
+        self._check(lib().pic_laser_preload(self.ctx))
 
     def get_fields(self):
         out = np.empty((9, self.nz_local, self.ny, self.nx), dtype=np.float64)
@@ -265,30 +300,42 @@ class Simulation:
 
 
 def workload_config(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
-                    sort_every=None, nccl_id=None, counts=None, migrate_capacity=0):
-    """pic_config for a synth.Workload (species q, m, w, dt from the workload).
+                    sort_every=None, nccl_id=None, counts=None, migrate_capacity=0, slab=None):
+    """pic_config for a synth.Workload (species q, m, w, dt, z boundary and
+    laser from the workload).
 
-    With nranks > 1 this rank holds the z slab [rank nz/nranks, (rank+1) nz/nranks)
-    and the default capacity leaves 10% headroom for migration."""
+    With nranks > 1 this rank holds the z slab `slab` = (lo, hi), default
+    [rank nz/nranks, (rank+1) nz/nranks), and the default capacity leaves 10%
+    headroom for migration."""
     species = [(s.q, s.m, s.w) for s in wl.species]
-    nz_local = wl.nz // nranks
+    if slab is None:
+        slab = (rank * (wl.nz // nranks), (rank + 1) * (wl.nz // nranks))
     if counts is None:
-        counts = [s.ppc * wl.nx * wl.ny * nz_local for s in wl.species]
+        zl, zh = slab
+        if getattr(wl, "plasma_z", None):
+            zl, zh = max(zl, wl.plasma_z[0]), min(zh, wl.plasma_z[1])
+        planes = max(0, zh - zl)
+        counts = [s.ppc * wl.nx * wl.ny * planes for s in wl.species]
         if nranks > 1:
             capacity_factor = max(capacity_factor, 1.1)
     cap = [max(1, int(np.ceil(c * capacity_factor))) for c in counts]
+    laser = None
+    if getattr(wl, "laser", None):
+        laser = dict(wl.laser)
     return make_config(wl.nx, wl.ny, wl.nz, species, wl.dt, wl.dx, wl.dy, wl.dz, wl.c, cap,
                        supercell or wl.supercell,
                        wl.sort_every if sort_every is None else sort_every,
-                       rank, nranks, flags, nccl_id, migrate_capacity)
+                       rank, nranks, flags, nccl_id, migrate_capacity,
+                       bc_z=BC_OPEN if getattr(wl, "open_z", False) else BC_PERIODIC,
+                       slab=slab if nranks > 1 else None, laser=laser)
 
 
 def simulation_from_workload(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
                              sort_every=None, nccl_id=None, counts=None, migrate_capacity=0,
-                             stream=None):
+                             stream=None, slab=None):
     """Build a Simulation for a synth.Workload."""
     cfg = workload_config(wl, capacity_factor, flags, rank, nranks, supercell, sort_every,
-                          nccl_id, counts, migrate_capacity)
+                          nccl_id, counts, migrate_capacity, slab)
     return Simulation(cfg, stream=stream)
 
 

@@ -61,6 +61,11 @@ class Workload:
     courant: float = 0.5
     nz_per_rank: int = 0        # C4: weak scaling, nz = nz_per_rank * nranks
     description: str = ""
+    # NEXT-1 (reading R21): open z box with the incident laser, and the z
+    # range [lo, hi) of planes that hold plasma (None: every plane)
+    open_z: bool = False
+    laser: tuple = ()           # (("e0", E0), ("omega", w), ("ramp", T), ("t0", t0), ("pol", (px, py)))
+    plasma_z: tuple = ()
 
     @property
     def dt(self) -> float:
@@ -93,6 +98,17 @@ def proton(ppc, sigma, density=N_E_DEFAULT, colocate_with=-1):
 
 _NC_C5 = (2.0 * math.pi / 32.0) ** 2 / (4.0 * math.pi)   # critical density, lambda = 32 cells
 
+
+def laser_c5(t0: float, a0: float = 10.0, wavelength: float = 32.0):
+    """BASELINE.json configs[4]: linearly polarised (x) plane wave of normalised
+    amplitude a0 = e E0 / (m c omega) and wavelength 32 cells, injected
+    through z = 0 (R21): E0 = a0 omega (e = m = c = 1), sin^2 ramp over two
+    wavelengths; t0 = the time it has been entering before t = 0 (its front
+    starts at z = c t0)."""
+    omega = 2.0 * math.pi / wavelength
+    return (("e0", a0 * omega), ("omega", omega), ("ramp", 2.0 * wavelength), ("t0", t0),
+            ("pol", (1.0, 0.0)))
+
 CONFIGS = {
     # BASELINE.json configs[0]
     "C1": Workload("C1", 16, 16, 16, (electron(8, 0.01),), steps=10, sort_every=5,
@@ -108,11 +124,19 @@ CONFIGS = {
     "C4": Workload("C4", 256, 256, 128, (electron(32, 0.1),), steps=100, sort_every=20,
                    nz_per_rank=128,
                    description="256x256x(128 N) thermal, 32 e/cell (268M per GPU), sigma 0.1"),
-    # BASELINE.json configs[4] -- laser-plasma slab (R18; literal source is NEXT-1)
+    # BASELINE.json configs[4] -- laser-plasma slab (NEXT-1, reading R21): open z,
+    # laser through z = 0 whose front has reached the slab surface z = 600 at t = 0,
+    # cold e + p slab (32 + 32 per cell, co-located, n = 10 n_c) on z in [600, 700)
     "C5": Workload("C5", 512, 512, 1024,
                    (electron(32, 0.0, 10 * _NC_C5), proton(32, 0.0, 10 * _NC_C5, colocate_with=0)),
-                   steps=500, sort_every=20,
-                   description="512x512x1024 laser-plasma slab z in [600,700), a0 = 10"),
+                   steps=500, sort_every=20, open_z=True, laser=laser_c5(600.0), plasma_z=(600, 700),
+                   description="512x512x1024 open-z laser-plasma slab z in [600,700), a0 = 10"),
+    # C5 on one GPU: the same columns (x, y periodic, the plane wave and the slab are
+    # uniform in x, y) on a 128 x 128 cross-section: 104.9M particles
+    "C5_1g": Workload("C5_1g", 128, 128, 1024,
+                      (electron(32, 0.0, 10 * _NC_C5), proton(32, 0.0, 10 * _NC_C5, colocate_with=0)),
+                      steps=500, sort_every=20, open_z=True, laser=laser_c5(600.0), plasma_z=(600, 700),
+                      description="C5 physics on a 128x128 cross-section (one GPU)"),
     # the paper's own benchmark: 40^3 grid,
     # 50 particles per cell, 1000 steps, frozen plasma (zero momenta, zero fields;
     # every stage still runs).  The paper's KNL time is 10.75 s = 3.36 ns/particle/step.
@@ -123,6 +147,11 @@ CONFIGS = {
                         description="8x12x16 non-cubic test grid"),
     "T_two_species": Workload("T_two_species", 12, 8, 8, (electron(3, 0.1), proton(3, 0.1)),
                               steps=4, sort_every=3, description="two-species test"),
+    # C5 in miniature (P18): open z, laser front on the slab surface at t = 0
+    "T_laser": Workload("T_laser", 8, 8, 96,
+                        (electron(2, 0.0, 10 * _NC_C5), proton(2, 0.0, 10 * _NC_C5, colocate_with=0)),
+                        steps=20, sort_every=5, open_z=True, laser=laser_c5(40.0), plasma_z=(40, 52),
+                        description="8x8x96 open-z laser-plasma slab z in [40,52), a0 = 10"),
 }
 
 

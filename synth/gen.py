@@ -7,7 +7,8 @@
 * R14 RNG: numpy Generator(PCG64(seed)), per species in order: first the
   positions rng.random((N,3)), then the momenta rng.normal(0, sigma_u, (N,3)).
   A rank of a z-slab decomposition draws its own slab with seed (seed, rank).
-Species with colocate_with >= 0 reuse that species' positions (C5, R13).
+Species with colocate_with >= 0 reuse that species' positions (C5, R13);
+a workload with plasma_z fills only those planes (C5, NEXT-1).
 
 Output per species: P float64[6][N] (rows x,y,z,ux,uy,uz), id uint64[N].
 """
@@ -28,6 +29,8 @@ def gen_species(wl: Workload, s: int, rng, z_lo: int = 0, z_hi: int | None = Non
                 positions=None, id_base: int = 0):
     sp = wl.species[s]
     z_hi = wl.nz if z_hi is None else z_hi
+    if wl.plasma_z:   # C5: plasma only on the planes [plasma_z[0], plasma_z[1])
+        z_lo, z_hi = max(z_lo, wl.plasma_z[0]), max(max(z_lo, wl.plasma_z[0]), min(z_hi, wl.plasma_z[1]))
     ncell = wl.nx * wl.ny * (z_hi - z_lo)
     n = ncell * sp.ppc
     P = np.empty((6, n), dtype=np.float64)

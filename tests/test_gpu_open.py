@@ -1,0 +1,209 @@
+"""GPU (libpic.so through the C ABI) vs the CPU oracle for the open-z box of
+SURVEY.md sec. 8f NEXT-1 (BASELINE.json configs[4]: laser injected through
+z = 0, absorbing z faces, a dense cold slab; reading R21 of DESIGN.md):
+first-order Mur faces with the incident wave, the t = 0 preload, particle
+absorption, and the z-slab decomposition with unequal (load-balanced)
+slabs whose ring is cut at the open faces.  Same tolerances as
+test_gpu_parity.py (north_star, BASELINE.json:5)."""
+import numpy as np
+import pytest
+
+from tests.helpers import compare_state, field_errs
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-12
+
+
+@pytest.fixture(scope="module")
+def pic():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1608_01009_b200 as P
+    P.lib()
+    return P
+
+
+def _oracle(O, wl, parts):
+    lz = dict(wl.laser)
+    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every,
+               bc_z=O.BC_OPEN, laser_e0=lz["e0"], laser_omega=lz["omega"], laser_ramp=lz["ramp"],
+               laser_t0=lz["t0"], laser_pol=tuple(lz["pol"]))
+    return O.Oracle(g, particles=[(p.copy(), i.copy()) for p, i in parts])
+
+
+def _L(wl):
+    return (wl.nx * wl.dx, wl.ny * wl.dy, wl.nz * wl.dz)
+
+
+def _check(sim, orc, wl, tol, what):
+    G = sim.get_fields()
+    errs = field_errs(G, orc.F)
+    for s in range(len(wl.species)):
+        gP, gi = sim.get_particles(s)
+        errs += list(compare_state(gP, gi, orc.P[s], orc.ids[s], _L(wl)))
+    assert max(errs) <= tol, (what, errs)
+    return max(errs)
+
+
+def test_vacuum_laser_injection_and_mur(pic, oracle_mod):
+    """No particles: the preloaded wave plus the wave entering through the
+    z = 0 face, 150 steps (the front crosses the top face z = 95 at step
+    ~190 of t0 = 40 ... so run past it with t0 = 80), E and B vs oracle."""
+    from synth import get_config
+    wl = get_config("T_laser").with_(species=get_config("T_laser").species[:1])
+    lz = dict(wl.laser)
+    lz["t0"] = 80.0
+    wl = wl.with_(laser=tuple(lz.items()))
+    orc = _oracle(oracle_mod, wl, [(np.zeros((6, 0)), np.zeros(0, np.uint64))])
+    orc.laser_preload()
+    sim = pic.simulation_from_workload(wl, counts=[1])
+    sim.laser_preload()
+    G = sim.get_fields()
+    assert max(field_errs(G[:6], orc.F[:6])) <= 1e-15
+    for n in range(150):
+        orc.step(1)
+        sim.step(1)
+        if n % 10 == 9:
+            G = sim.get_fields()
+            assert max(field_errs(G, orc.F)) <= TOL_STEP, n
+    assert np.abs(orc.F[0, -1]).max() > 0.1 * lz["e0"]   # the wave did reach the top face
+
+
+def test_laser_plasma_teacher_forced(pic, oracle_mod):
+    """C5 in miniature (P18): relativistic electrons in the a0 = 10 wave,
+    every step started from the oracle's state, 12 steps <= 1e-12."""
+    from synth import gen_particles, get_config
+    wl = get_config("T_laser")
+    parts = gen_particles(wl)
+    orc = _oracle(oracle_mod, wl, parts)
+    orc.laser_preload()
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for step in range(12):
+        sim.set_fields(orc.F[:6].copy())
+        for s in range(2):
+            sim.set_particles(s, orc.P[s], orc.ids[s])
+        orc.step(1)
+        sim.step(1)
+        _check(sim, orc, wl, TOL_STEP, step)
+    umax = np.abs(orc.P[0][3:]).max()
+    assert umax > 1.0, umax   # relativistic
+
+
+def test_laser_plasma_free_running(pic, oracle_mod):
+    """20 free-running steps with sorts (K = 5): <= 1e-10."""
+    from synth import gen_particles, get_config
+    wl = get_config("T_laser")
+    parts = gen_particles(wl)
+    orc = _oracle(oracle_mod, wl, parts)
+    orc.laser_preload()
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    sim.laser_preload()
+    worst = 0.0
+    for step in range(20):
+        orc.step(1)
+        sim.step(1)
+        worst = max(worst, _check(sim, orc, wl, 1e-10, step))
+
+
+@pytest.mark.parametrize("where", ["bottom", "top"])
+def test_absorption_on_gpu(pic, oracle_mod, where):
+    """Fast particles crossing the open faces are removed (the others keep
+    their state), their current up to the face is deposited and the rest
+    dropped -- as in the oracle (pinned in test_oracle_open.py)."""
+    from synth import get_config
+    wl = get_config("T_laser").with_(species=get_config("T_laser").species[:1])
+    lz = dict(wl.laser)
+    lz["e0"] = 0.0
+    wl = wl.with_(laser=tuple(lz.items()), nz=32)
+    rng = np.random.default_rng(31)
+    n = 400
+    P = np.zeros((6, n))
+    P[0] = rng.random(n) * wl.nx
+    P[1] = rng.random(n) * wl.ny
+    zmax = wl.nz - 1
+    if where == "bottom":
+        P[2] = rng.random(n) * 1.5
+        P[5] = -rng.random(n) * 3.0
+    else:
+        P[2] = zmax - rng.random(n) * 1.5
+        P[5] = rng.random(n) * 3.0
+    P[3:5] = rng.normal(0, 0.3, (2, n))
+    ids = np.arange(n, dtype=np.uint64)
+    orc = _oracle(oracle_mod, wl, [(P, ids)])
+    sim = pic.simulation_from_workload(wl, counts=[n])
+    sim.set_particles(0, P, ids)
+    for step in range(4):
+        orc.step(1)
+        sim.step(1)
+        _check(sim, orc, wl, TOL_STEP, step)
+    assert orc.P[0].shape[1] < n // 2   # most of them left
+
+
+def test_open_config_errors(pic):
+    """Open-z API contract: positions beyond the top face, preload on a
+    periodic box or after a step, diagnostics on an open box."""
+    from synth import get_config
+    wl = get_config("T_laser")
+    sim = pic.simulation_from_workload(wl, counts=[4, 4])
+    P = np.zeros((6, 1))
+    P[2] = wl.nz - 0.5          # inside [0, L) but beyond zmax = (nz - 1) dz
+    with pytest.raises(pic.PicError):
+        sim.set_particles(0, P, np.zeros(1, np.uint64))
+    with pytest.raises(pic.PicError):
+        sim.diagnostics()
+    sim.step(1)
+    with pytest.raises(pic.PicError):
+        sim.laser_preload()
+    per = pic.simulation_from_workload(get_config("C1"), counts=[4])
+    with pytest.raises(pic.PicError):
+        per.laser_preload()
+
+
+@pytest.mark.parametrize("split", [(0, 40, 52, 96), "balanced"])
+def test_open_unequal_slabs_match_single_domain_oracle(pic, oracle_mod, split):
+    """Slab group on one GPU (PIC_FLAG_LOCAL_GROUP): three unequal z slabs,
+    the ring cut at the open faces (no exchange between the top and the
+    bottom rank), against the single-domain oracle; the balanced split comes
+    from pic_balance_slabs with a particles + cells cost per plane."""
+    import torch
+    from synth import gen_particles, get_config
+    wl = get_config("T_laser")
+    parts = gen_particles(wl)
+    if split == "balanced":
+        zc = np.zeros(wl.nz)
+        for P, _ in parts:
+            zc += np.bincount(np.floor(P[2]).astype(int), minlength=wl.nz)
+        cost = zc + 0.3 * wl.nx * wl.ny
+        split = pic.balance_slabs(wl.nz, 3, wl.supercell, 4, cost)
+    orc = _oracle(oracle_mod, wl, parts)
+    orc.laser_preload()
+    stream = torch.cuda.Stream()
+    sims = []
+    for r in range(3):
+        lo, hi = split[r], split[r + 1]
+        planes = max(0, min(hi, wl.plasma_z[1]) - max(lo, wl.plasma_z[0]))
+        cnt = [max(64, int(2 * s.ppc * wl.nx * wl.ny * max(planes, 4))) for s in wl.species]
+        cfg = pic.workload_config(wl, rank=r, nranks=3, flags=pic.FLAG_LOCAL_GROUP, counts=cnt,
+                                  migrate_capacity=4096, slab=(lo, hi))
+        sims.append(pic.Simulation(cfg, stream=stream))
+    for r, sim in enumerate(sims):
+        for s, (P, ids) in enumerate(parts):
+            sim.set_particles(s, P, ids)
+        sim.laser_preload()
+    for step in range(16):
+        orc.step(1)
+        pic.step_group(sims, 1)
+        G = np.concatenate([s.get_fields() for s in sims], axis=1)
+        errs = field_errs(G, orc.F)
+        for s in range(2):
+            Ps, Is = zip(*[sim.get_particles(s) for sim in sims])
+            errs += list(compare_state(np.concatenate(Ps, axis=1), np.concatenate(Is),
+                                       orc.P[s], orc.ids[s], _L(wl)))
+            for r, P_r in enumerate(Ps):   # every particle lives in its rank's slab
+                assert (P_r[2] >= split[r]).all() and (P_r[2] < split[r + 1]).all()
+        assert max(errs) <= 1e-10, (step, errs)
