@@ -147,10 +147,12 @@ CONFIGS = {
                         description="8x12x16 non-cubic test grid"),
     "T_two_species": Workload("T_two_species", 12, 8, 8, (electron(3, 0.1), proton(3, 0.1)),
                               steps=4, sort_every=3, description="two-species test"),
-    # C5 in miniature (P18): open z, laser front on the slab surface at t = 0
+    # C5 in miniature (P18): open z; the laser's sin^2 ramp (64 = 2 lambda) has
+    # just passed the slab surface z = 40 at t = 0, so the electrons turn
+    # relativistic within a few steps
     "T_laser": Workload("T_laser", 8, 8, 96,
                         (electron(2, 0.0, 10 * _NC_C5), proton(2, 0.0, 10 * _NC_C5, colocate_with=0)),
-                        steps=20, sort_every=5, open_z=True, laser=laser_c5(40.0), plasma_z=(40, 52),
+                        steps=20, sort_every=5, open_z=True, laser=laser_c5(104.0), plasma_z=(40, 52),
                         description="8x8x96 open-z laser-plasma slab z in [40,52), a0 = 10"),
 }
 

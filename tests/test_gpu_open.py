@@ -8,7 +8,7 @@ test_gpu_parity.py (north_star, BASELINE.json:5)."""
 import numpy as np
 import pytest
 
-from tests.helpers import compare_state, field_errs
+from tests.helpers import compare_state
 
 pytestmark = pytest.mark.gpu
 
@@ -38,9 +38,20 @@ def _L(wl):
     return (wl.nx * wl.dx, wl.ny * wl.dy, wl.nz * wl.dz)
 
 
+def field_errs_grouped(G, F):
+    """Reading R17 for the laser runs: the x-polarised wave dominates E and B
+    by up to 12 orders of magnitude over the plasma's response in the other
+    components (whose per-array maxima are then rounding noise), so E and B
+    errors are relative to max |E, B| over all six components, J errors to
+    max |J| over its three."""
+    se = max(np.abs(F[:6]).max(), 1e-300)
+    sj = max(np.abs(F[6:]).max(), 1e-300)
+    return [float(np.abs(G[c] - F[c]).max() / (se if c < 6 else sj)) for c in range(9)]
+
+
 def _check(sim, orc, wl, tol, what):
     G = sim.get_fields()
-    errs = field_errs(G, orc.F)
+    errs = field_errs_grouped(G, orc.F)
     for s in range(len(wl.species)):
         gP, gi = sim.get_particles(s)
         errs += list(compare_state(gP, gi, orc.P[s], orc.ids[s], _L(wl)))
@@ -49,9 +60,9 @@ def _check(sim, orc, wl, tol, what):
 
 
 def test_vacuum_laser_injection_and_mur(pic, oracle_mod):
-    """No particles: the preloaded wave plus the wave entering through the
-    z = 0 face, 150 steps (the front crosses the top face z = 95 at step
-    ~190 of t0 = 40 ... so run past it with t0 = 80), E and B vs oracle."""
+    """No particles: the preloaded wave (front at z = 80) plus the wave
+    entering through the z = 0 face, 150 steps; the front leaves through the
+    top face z = 95 after ~52 steps.  E and B vs oracle."""
     from synth import get_config
     wl = get_config("T_laser").with_(species=get_config("T_laser").species[:1])
     lz = dict(wl.laser)
@@ -62,13 +73,13 @@ def test_vacuum_laser_injection_and_mur(pic, oracle_mod):
     sim = pic.simulation_from_workload(wl, counts=[1])
     sim.laser_preload()
     G = sim.get_fields()
-    assert max(field_errs(G[:6], orc.F[:6])) <= 1e-15
+    assert max(field_errs_grouped(G, orc.F)[:6]) <= 1e-15
     for n in range(150):
         orc.step(1)
         sim.step(1)
         if n % 10 == 9:
             G = sim.get_fields()
-            assert max(field_errs(G, orc.F)) <= TOL_STEP, n
+            assert max(field_errs_grouped(G, orc.F)) <= TOL_STEP, n
     assert np.abs(orc.F[0, -1]).max() > 0.1 * lz["e0"]   # the wave did reach the top face
 
 
@@ -108,6 +119,8 @@ def test_laser_plasma_free_running(pic, oracle_mod):
         orc.step(1)
         sim.step(1)
         worst = max(worst, _check(sim, orc, wl, 1e-10, step))
+    assert np.abs(orc.P[0][3:]).max() > 2.0   # relativistic electrons
+    print(f"free-running worst relative error {worst:.2e}")
 
 
 @pytest.mark.parametrize("where", ["bottom", "top"])
@@ -199,7 +212,7 @@ def test_open_unequal_slabs_match_single_domain_oracle(pic, oracle_mod, split):
         orc.step(1)
         pic.step_group(sims, 1)
         G = np.concatenate([s.get_fields() for s in sims], axis=1)
-        errs = field_errs(G, orc.F)
+        errs = field_errs_grouped(G, orc.F)
         for s in range(2):
             Ps, Is = zip(*[sim.get_particles(s) for sim in sims])
             errs += list(compare_state(np.concatenate(Ps, axis=1), np.concatenate(Is),
