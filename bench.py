@@ -134,6 +134,43 @@ def reduce_sum_over_ranks(v: float) -> float:
     return float(t.item())
 
 
+# per-plane cost of the static load balance (NEXT-1): time per particle-step
+# and per cell-step in particle-step units (B200: 0.055 ns per particle
+# (C3 particle kernel + sort), 0.064 ns per cell (C3 field stage))
+CELL_COST = 1.2
+
+
+def slab_split(wl, world):
+    """z cut planes of the world ranks: uniform nz/world, or -- for a workload
+    whose plasma fills only part of the box (C5) -- pic_balance_slabs on
+    particles + CELL_COST x cells per plane."""
+    if world == 1 or not wl.plasma_z:
+        return [r * (wl.nz // world) for r in range(world)] + [wl.nz]
+    import paper_1608_01009_b200 as pkg
+    ppc = sum(s.ppc for s in wl.species)
+    cost = np.full(wl.nz, CELL_COST * wl.nx * wl.ny)
+    cost[wl.plasma_z[0]:wl.plasma_z[1]] += ppc * wl.nx * wl.ny
+    return pkg.balance_slabs(wl.nz, world, wl.supercell, max(4, wl.supercell), cost)
+
+
+def occupied_cells(wl, lo, hi):
+    """Cells of the planes [lo, hi) that hold particles (the E/B tile gather
+    and the J flush of the particle kernel touch only those)."""
+    if wl.plasma_z:
+        lo, hi = max(lo, wl.plasma_z[0]), min(hi, wl.plasma_z[1])
+    return wl.nx * wl.ny * max(0, hi - lo)
+
+
+def oracle_grid(O, wl):
+    lz = dict(wl.laser) if wl.laser else {}
+    return O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+                  [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every,
+                  bc_z=O.BC_OPEN if wl.open_z else O.BC_PERIODIC,
+                  laser_e0=lz.get("e0", 0.0), laser_omega=lz.get("omega", 0.0),
+                  laser_ramp=lz.get("ramp", 0.0), laser_t0=lz.get("t0", 0.0),
+                  laser_pol=tuple(lz.get("pol", (1.0, 0.0))))
+
+
 def pinned_copy(P, ids):
     import torch
     tp = torch.empty(P.shape, dtype=torch.float64, pin_memory=True)
@@ -149,8 +186,7 @@ def oracle_sample_rate(wl, parts, target_s=10.0, max_particles=None):
     contiguous particle sample pushed through one oracle step."""
     from oracle import oracle as O
     O.build()
-    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
-               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every)
+    g = oracle_grid(O, wl)
     sub = []
     n_tot = sum(p.shape[1] for p, _ in parts)
     frac = 1.0 if max_particles is None else min(1.0, max_particles / n_tot)
@@ -158,6 +194,8 @@ def oracle_sample_rate(wl, parts, target_s=10.0, max_particles=None):
         k = max(1, int(P.shape[1] * frac))
         sub.append((P[:, :k].copy(), ids[:k].copy()))
     orc = O.Oracle(g, particles=sub)
+    if wl.laser:
+        orc.laser_preload()
     n_sample = sum(p.shape[1] for p, _ in sub)
     t0 = time.perf_counter()
     steps = 0
@@ -179,14 +217,15 @@ def run_reference(args, wl, rank, world):
     parts = gen_particles(wl)
     from oracle import oracle as O
     O.build()
-    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
-               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every)
+    g = oracle_grid(O, wl)
     n_sample = args.ref_sample
     sub = []
     for P, ids in parts:
         k = min(P.shape[1], max(1, n_sample // len(parts)))
         sub.append((P[:, :k].copy(), ids[:k].copy()))
     orc = O.Oracle(g, particles=sub)
+    if wl.laser:
+        orc.laser_preload()
     ns = sum(p.shape[1] for p, _ in sub)
     for _ in range(args.warmup):
         orc.step(1)
@@ -199,7 +238,7 @@ def run_reference(args, wl, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "ns_per_particle_step": 1e9 / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": wl_config(wl, world),
+        "config": wl_config(wl, world, slab_split(wl, world)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"first {ns} particles of {wl.name} (of {wl.n_particles}) "
                                    f"through full oracle steps (fields on the whole grid), "
@@ -209,13 +248,20 @@ def run_reference(args, wl, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def wl_config(wl, world):
-    return {"workload": wl.name, "grid": [wl.nx, wl.ny, wl.nz],
-            "particles": wl.n_particles, "species": len(wl.species),
-            "ppc": sum(s.ppc for s in wl.species), "sort_every": wl.sort_every,
-            "supercell": wl.supercell, "dt": wl.dt,
-            "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
-            "l2": "inputs larger than L2 (particle state > 126 MB), no flush"}
+def wl_config(wl, world, split=None):
+    c = {"workload": wl.name, "grid": [wl.nx, wl.ny, wl.nz],
+         "particles": wl.n_particles, "species": len(wl.species),
+         "ppc": sum(s.ppc for s in wl.species), "sort_every": wl.sort_every,
+         "supercell": wl.supercell, "dt": wl.dt,
+         "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+         "l2": "inputs larger than L2 (particle state > 126 MB), no flush"}
+    if wl.open_z:
+        lz = dict(wl.laser)
+        c["boundary"] = (f"open z (first-order Mur), laser e0={lz['e0']:.4f} omega={lz['omega']:.4f} "
+                         f"t0={lz['t0']} ramp={lz['ramp']}, plasma z in {list(wl.plasma_z)}")
+    if split is not None and world > 1:
+        c["slabs"] = list(split)
+    return c
 
 
 def run_ours(args, wl, rank, world, local):
@@ -230,15 +276,23 @@ def run_ours(args, wl, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         nccl_id = pkg.broadcast_nccl_id(pkg.nccl_unique_id() if rank == 0 else bytes(128))
-        nzl = wl.nz // world
-        parts = gen_particles(wl, rank=rank, z_lo=rank * nzl, z_hi=(rank + 1) * nzl)
+    split = slab_split(wl, world)
+    slab = (split[rank], split[rank + 1])
+    if world > 1:
+        parts = gen_particles(wl, rank=rank, z_lo=slab[0], z_hi=slab[1])
     else:
         parts = gen_particles(wl)
     n_local = sum(p.shape[1] for p, _ in parts)
 
     def new_sim(flags=0):
         return pkg.simulation_from_workload(wl, capacity_factor=1.0, flags=flags, rank=rank,
-                                            nranks=world, nccl_id=nccl_id)
+                                            nranks=world, nccl_id=nccl_id, slab=slab)
+
+    def load(sim, ps):
+        for s, (P, ids) in enumerate(ps):
+            sim.set_particles(s, P, ids)
+        if wl.laser and sim.step_index() == 0:
+            sim.laser_preload()   # C5: the wave that entered through z = 0 before t = 0
 
     def barrier():
         if world > 1:
@@ -247,8 +301,7 @@ def run_ours(args, wl, rank, world, local):
 
     # ---------------- device-resident timed region (value)
     sim = new_sim()
-    for s, (P, ids) in enumerate(parts):
-        sim.set_particles(s, P, ids)
+    load(sim, parts)
     sim.step(args.warmup)
     sim.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -271,8 +324,7 @@ def run_ours(args, wl, rank, world, local):
 
     # ---------------- profiled pass: per-stage CUDA events around each launch
     psim = new_sim(pkg.FLAG_PROFILE)
-    for s, (P, ids) in enumerate(parts):
-        psim.set_particles(s, P, ids)
+    load(psim, parts)
     psim.step(args.warmup)
     psim.stage_times()
     psim.step(args.steps)
@@ -280,7 +332,7 @@ def run_ours(args, wl, rank, world, local):
     psim.close()
     del psim
     torch.cuda.empty_cache()
-    ppc_cells = wl.nx * wl.ny * (wl.nz // world)
+    ppc_cells = occupied_cells(wl, slab[0], slab[1])
     alg_bytes_total = sum(p.shape[1] for p, _ in parts) * 96.0 + len(parts) * ppc_cells * 72.0
     n_launch = max(st["particle_launches"], 1)
     per_launch_ms = st["particle"] / n_launch
@@ -304,8 +356,7 @@ def run_ours(args, wl, rank, world, local):
         pinned = [pinned_copy(P, ids) for P, ids in parts]
         outs = [(np.empty_like(P), np.empty_like(ids)) for P, ids in parts]
         esim = new_sim()
-        for s, (_, _, Pn, In) in enumerate(pinned):
-            esim.set_particles(s, Pn, In)
+        load(esim, [(Pn, In) for _, _, Pn, In in pinned])
         esim.step(args.warmup)
         barrier()
         torch.cuda.synchronize()
@@ -342,7 +393,7 @@ def run_ours(args, wl, rank, world, local):
             "vs_baseline": value / PAPER_KNL_FROZEN if wl.name == "FROZEN" else None,
             "dtype": "f64",
             "data": "synthetic (seeded numpy PCG64, DESIGN.md sec. 6)",
-            "config": wl_config(wl, world),
+            "config": wl_config(wl, world, split),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "particle (gather+Boris+VB deposit)",

@@ -77,7 +77,8 @@ class Workload:
 
     @property
     def n_particles(self) -> int:
-        return sum(s.ppc for s in self.species) * self.ncells
+        planes = (self.plasma_z[1] - self.plasma_z[0]) if self.plasma_z else self.nz
+        return sum(s.ppc for s in self.species) * self.nx * self.ny * planes
 
     def for_ranks(self, nranks: int) -> "Workload":
         if self.nz_per_rank:

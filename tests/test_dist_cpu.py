@@ -44,6 +44,13 @@ def _worker(rank, world, port, results):
     cfg = pkg.workload_config(wl, rank=rank, nranks=world, nccl_id=uid)
     nb = C.c_size_t(0)
     rc = pkg.lib().pic_workspace_size(C.byref(cfg), C.byref(nb))
+    # C5 (NEXT-1): balanced unequal slabs of an open box, ring cut at the faces
+    wl5 = get_config("C5")
+    split = bench.slab_split(wl5, world)
+    cfg5 = pkg.workload_config(wl5, rank=rank, nranks=world, nccl_id=uid,
+                               slab=(split[rank], split[rank + 1]))
+    rc5 = pkg.lib().pic_workspace_size(C.byref(cfg5), C.byref(C.c_size_t(0)))
+    results[(rank, "c5")] = (list(split), rc5, int(cfg5.slab_lo), int(cfg5.slab_hi), int(cfg5.bc_z))
     t_max = bench.reduce_max_over_ranks(float(rank + 1))
     n_tot = bench.reduce_sum_over_ranks(float(10 * (rank + 1)))
     results[rank] = (uid, rc, nb.value, int(cfg.capacity[0]), int(cfg.nz), t_max, n_tot)
@@ -72,3 +79,8 @@ def test_two_rank_slab_setup_over_gloo():
     assert r0[4] == 256                                   # global nz = 128 per rank
     assert r0[5] == r1[5] == 2.0                          # max over ranks
     assert r0[6] == r1[6] == 30.0                         # sum over ranks
+    c0, c1 = results[(0, "c5")], results[(1, "c5")]
+    assert c0[0] == c1[0] and c0[0][0] == 0 and c0[0][-1] == 1024
+    assert c0[1] == c1[1] == 0 and c0[4] == 1              # valid open-z configs
+    assert (c0[2], c0[3]) == (0, c0[0][1]) and (c1[2], c1[3]) == (c0[0][1], 1024)
+    assert 600 < c0[0][1] < 700                           # the cut falls inside the slab
