@@ -189,7 +189,9 @@ def oracle_sample_rate(wl, parts, target_s=10.0, max_particles=None):
     g = oracle_grid(O, wl)
     sub = []
     n_tot = sum(p.shape[1] for p, _ in parts)
-    frac = 1.0 if max_particles is None else min(1.0, max_particles / n_tot)
+    if max_particles is None:   # ~0.4 us per particle-step single threaded: bound the sample
+        max_particles = int(target_s * 1.0e6)
+    frac = min(1.0, max_particles / n_tot)
     for P, ids in parts:
         k = max(1, int(P.shape[1] * frac))
         sub.append((P[:, :k].copy(), ids[:k].copy()))

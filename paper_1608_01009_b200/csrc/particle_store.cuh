@@ -7,12 +7,21 @@
 
 namespace pic {
 
-// returns true when the particle migrated (slot now dead)
+// returns true when the particle migrated (slot now dead).  kGeneral =
+// false compiles the single-domain periodic store only (no slab or open-box
+// branches; the kernels pick it when nranks == 1 and z is periodic).
+template <bool kGeneral = true>
 __device__ __forceinline__ bool store_particle(const GridDev &g, const SpeciesDev &sp,
                                                const ParticlesDev &out, const uint64_t *in_id,
                                                int64_t p, double x, double y, double z, double ux,
                                                double uy, double uz, bool copy_id, unsigned *err)
 {
+    if constexpr (!kGeneral) {
+        out.x[p] = x; out.y[p] = y; out.z[p] = z;
+        out.ux[p] = ux; out.uy[p] = uy; out.uz[p] = uz;
+        if (copy_id) out.id[p] = in_id[p];
+        return false;
+    }
     if (g.open_z && !(z >= 0.0 && z < g.zmax)) {
         // NEXT-1: left the open box through z = 0 or z = zmax (its current up to
         // the face is deposited): absorbed, the slot is dead until the next sort

@@ -9,6 +9,7 @@
 
 namespace pic {
 
+template <bool kGeneral = true>
 __device__ __forceinline__ void push_one_global(const GridDev &g, const double *__restrict__ EB,
                                                 double *__restrict__ J, const SpeciesDev &sp,
                                                 double &x, double &y, double &z, double &ux,
@@ -68,7 +69,7 @@ __device__ __forceinline__ void push_one_global(const GridDev &g, const double *
     }
     x = wrap_coord(xn, g.Lx);
     y = wrap_coord(yn, g.Ly);
-    z = wrap_z(g, zn);
+    z = kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz);
 }
 
 }  // namespace pic

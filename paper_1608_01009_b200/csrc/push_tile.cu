@@ -77,12 +77,13 @@ constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
 constexpr int64_t kMaxTileParticles = 16383;
 
 // rare path: a particle outside its tile (drifted > H cells since the sort)
+template <bool kGeneral>
 __device__ __forceinline__ void push_outside_tile(const GridDev &g, const double *EB, double *J,
                                                   const SpeciesDev &sp, double &x, double &y,
                                                   double &z, double &ux, double &uy, double &uz,
                                                   unsigned *err)
 {
-    push_one_global(g, EB, J, sp, x, y, z, ux, uy, uz, err);
+    push_one_global<kGeneral>(g, EB, J, sp, x, y, z, ux, uy, uz, err);
 }
 
 // Deposits one in-cell segment P1 -> P2 (local coordinates of the cell whose
@@ -176,7 +177,9 @@ __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *
     }
 }
 
-template <int S, int H>
+// kGeneral: slabs (nranks > 1) or an open z box (migration / absorption
+// in the final store); false for the single-domain periodic box
+template <int S, int H, bool kGeneral>
 __global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
 k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
             double *__restrict__ J, ParticlesDev in, ParticlesDev out,
@@ -304,10 +307,10 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
             u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
             if (ok)
-                store_particle(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
-                               wrap_z(g, zn), ux, uy, uz, copy_id != 0, err);
+                store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
+                               kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, copy_id != 0, err);
             else
-                store_particle(g, sp, out, in.id, p, x, y, z, ux, uy, uz, copy_id != 0, err);
+                store_particle<kGeneral>(g, sp, out, in.id, p, x, y, z, ux, uy, uz, copy_id != 0, err);
             if (ok) {
                 const int jbase = tx + JPX * ty + JPY * tz;
                 double ex_, ey_, ez_, r1[3], r2[3];
@@ -341,8 +344,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                 fq[slot] = (unsigned)p;
             } else {
                 double xx = x, yy = y, zz = z;
-                push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
-                store_particle(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
+                push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+                store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
                 u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
             }
         }
@@ -357,8 +360,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     for (int e = tid; e < nf; e += NT) {
         const int p = (int)fq[e];
         double xx = in.x[p], yy = in.y[p], zz = in.z[p], ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
-        push_outside_tile(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
-        store_particle(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
+        push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+        store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
         u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
     }
     __syncthreads();
@@ -396,7 +399,7 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
     if (n > 0) k_u2max<<<296, 256, 0, st>>>(P, n, out);
 }
 
-template <int S, int H>
+template <int S, int H, bool kGeneral>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
                         const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
                         const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
@@ -409,7 +412,7 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
     // splitting C2's 3200-particle supercells was measured slower (extra tile
     // loads and flushes outweigh the shorter last wave)
     const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + 8191) / 8192));
-    k_push_tile<S, H><<<nsc * split, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
+    k_push_tile<S, H, kGeneral><<<nsc * split, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
                                                                copy_id ? 1 : 0, split, err);
 }
 
@@ -426,9 +429,13 @@ void tile_box(int S, int box[4])
 
 void configure_tile_kernels()
 {
-    cudaFuncSetAttribute(k_push_tile<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_push_tile<4, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)TileGeom<4, 1>::smem_bytes);
-    cudaFuncSetAttribute(k_push_tile<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_push_tile<2, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TileGeom<2, 1>::smem_bytes);
+    cudaFuncSetAttribute(k_push_tile<4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TileGeom<4, 1>::smem_bytes);
+    cudaFuncSetAttribute(k_push_tile<2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)TileGeom<2, 1>::smem_bytes);
 }
 
@@ -437,10 +444,15 @@ void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB
                       const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
                       cudaStream_t st)
 {
-    if (g.S == 4)
-        launch_tile<4, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+    const bool general = g.nranks > 1 || g.open_z;
+    if (g.S == 4 && general)
+        launch_tile<4, 1, true>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+    else if (g.S == 4)
+        launch_tile<4, 1, false>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+    else if (g.S == 2 && general)
+        launch_tile<2, 1, true>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
     else if (g.S == 2)
-        launch_tile<2, 1>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+        launch_tile<2, 1, false>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
 }
 
 }  // namespace pic
