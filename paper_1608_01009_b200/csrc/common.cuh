@@ -82,6 +82,11 @@ struct SpeciesDev {
     // the fixed-point scale of the deposit tile (push_tile.cu).
     const unsigned *u2max_in;
     unsigned *u2max_out;
+    // per-launch constants of the fused kernel (computed once, not per CTA):
+    // VB flux factors q w / (dt dA) per axis (host) and the fixed-point scale
+    // 2^F, 2^-F of the J tile (k_step_prep on the device, from u2max_in)
+    double kx, ky, kz;
+    const double *scale;   // [2]: 2^F, 2^-F
     MigrateDev mig;
 };
 

@@ -37,6 +37,14 @@ void launch_push_tail(const GridDev &g, const double *EB, double *J, const Parti
 // ---- push_tile.cu : fused supercell kernel ----
 bool tile_supported(int S);
 void tile_box(int S, int box[4]);   // TMA box of the E/B tile (x pitch, y, z, comps)
+// per step: fixed-point J-tile scale per species from u2max_in, u2max_out = 0
+struct StepPrep {
+    int n_species;
+    double qw[4];
+    double c, dV;
+};
+void launch_step_prep(const unsigned *u2max_in, unsigned *u2max_out, double *scale, const StepPrep &p,
+                      cudaStream_t st);
 // max |u|^2 of n particles -> *out (high 32 bits of the fp64 value)
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st);
 void configure_tile_kernels();

@@ -103,9 +103,11 @@ __device__ __forceinline__ void boris(double h, double ex, double ey, double ez,
 // that rounds to L becomes 0.
 __device__ __forceinline__ double wrap_coord(double x, double L)
 {
-    const double lo = x + L;   // selects, no branches
-    const double wl = (lo == L) ? 0.0 : lo;
-    return (x >= L) ? x - L : ((x < 0.0) ? wl : x);
+    // almost every particle stays inside: one test, the rare wrap in a branch
+    if (!(x < 0.0 || x >= L)) return x;
+    if (x >= L) return x - L;
+    const double lo = x + L;
+    return (lo == L) ? 0.0 : lo;
 }
 
 // z after a move: periodic wrap (R7), or unchanged in an open box (NEXT-1;

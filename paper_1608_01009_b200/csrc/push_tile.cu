@@ -201,13 +201,19 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     const int tid = threadIdx.x, lane = tid & 31;
     // `split` CTAs share a supercell, each taking a contiguous part of its
     // particles (short grids fill the last wave; each CTA has its own tiles)
-    const int sc = blockIdx.x / split, part = blockIdx.x % split;
+    // grid = (nsx * split, nsy, nsz): no integer divisions on the common path
+    const int scx = split == 1 ? (int)blockIdx.x : (int)blockIdx.x / split;
+    const int part = split == 1 ? 0 : (int)blockIdx.x % split;
+    const int scy = blockIdx.y, scz = blockIdx.z;
+    const int sc = scx + g.nsx * (scy + g.nsy * scz);
     const int P0 = (int)sc_off[sc], P1 = (int)sc_off[sc + 1];
-    const int p0 = P0 + (int)(((int64_t)(P1 - P0) * part) / split);
-    const int p1 = P0 + (int)(((int64_t)(P1 - P0) * (part + 1)) / split);
+    int p0 = P0, p1 = P1;
+    if (split > 1) {
+        p0 = P0 + (int)(((int64_t)(P1 - P0) * part) / split);
+        p1 = P0 + (int)(((int64_t)(P1 - P0) * (part + 1)) / split);
+    }
     if (p0 == p1) return;   // empty (uniform per CTA)
 
-    const int scx = sc % g.nsx, scy = (sc / g.nsx) % g.nsy, scz = sc / (g.nsx * g.nsy);
     // local-grid coordinates of the tile origin (same for the E/B and J tiles)
     const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
     const int64_t gorigin = pidx(g, ox, oy, oz);   // padded global index of tile node (0,0,0)
@@ -215,9 +221,21 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     if (tid == 0) {
         mbar_init(bar_eb, 1);
         fence_mbar_init();
+#ifndef PIC_EXP_NOTMA
         mbar_arrive_expect_tx(bar_eb, 6 * NE * sizeof(double));
         tma_load_4d(eb, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, bar_eb);
+#endif
     }
+#ifdef PIC_PF_L2
+    if (tid < 6) {
+        // the CTA's whole particle range into L2 up front: the per-thread
+        // staging below then waits on L2, not HBM, latency
+        const double *arr = tid == 0 ? in.x : tid == 1 ? in.y : tid == 2 ? in.z : tid == 3 ? in.ux : tid == 4 ? in.uy : in.uz;
+        const uintptr_t a0 = (uintptr_t)(arr + p0) & ~(uintptr_t)15;
+        const uintptr_t a1 = ((uintptr_t)(arr + p1) + 15) & ~(uintptr_t)15;
+        prefetch_l2_bulk((const void *)a0, (unsigned)(a1 - a0));
+    }
+#endif
     auto stage = [&](int p, int st) {   // this thread's particle p -> its staging slot
         double *d = pbuf + st * 6 * NT + tid;
         cp_async8(d + 0 * NT, in.x + p);
@@ -231,7 +249,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     cp_async_commit();
     {   // zero the fixed-point J tile (16-byte stores)
         uint4 *j4 = (uint4 *)jt;
+#ifndef PIC_EXP_NOZERO
         for (int t = tid; t < (9 * NJ) / 4; t += NT) j4[t] = make_uint4(0u, 0u, 0u, 0u);
+#endif
         for (int t = (9 * NJ) / 4 * 4 + tid; t < 9 * NJ; t += NT) jt[t] = 0u;
     }
     if (tid == 0) {
@@ -239,26 +259,16 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         *fqcount = 0u;
     }
 
-    const double kx = sp.qw / (g.dt * g.dy * g.dz);
-    const double ky = sp.qw / (g.dt * g.dx * g.dz);
-    const double kz = sp.qw / (g.dt * g.dx * g.dy);
+    const double kx = sp.kx, ky = sp.ky, kz = sp.kz;   // q w / (dt dA), host
     const double cdt = g.c * g.dt;
-    // fixed-point scale 2^F of this step: every contribution is bounded by
-    // |qw| c beta / (dx dy dz) * 13/12 with beta <= 2 x the largest beta of
-    // the previous step (from its max |u|^2); 2^F maps that bound to < 2^46
-    double scale, inv_scale;
-    {
-        const double u2 = __longlong_as_double(((unsigned long long)(*sp.u2max_in) << 32) | 0xffffffffull);
-        const double beta = fmax(1e-4, fmin(1.0, 2.0 * sqrt(u2 / (1.0 + u2))));
-        const double wmax = fabs(sp.qw) * g.c / (g.dx * g.dy * g.dz) * (13.0 / 12.0) * beta;
-        const int F = wmax > 0.0 ? min(1000, (int)floor(46.0 - log2(wmax))) : 1000;
-        scale = ldexp(1.0, F);
-        inv_scale = ldexp(1.0, -F);
-    }
+    // fixed-point scale 2^F of this step (k_step_prep, once per launch)
+    const double scale = sp.scale[0], inv_scale = sp.scale[1];
     double u2loc = 0.0;   // this thread's max |u|^2 after the push
     const bool tile_ok = (p1 - p0) <= kMaxTileParticles;   // else the counters could overflow
     __syncthreads();
+#ifndef PIC_EXP_NOTMA
     mbar_wait(bar_eb, 0);
+#endif
 
     int st = 0;
     for (int p = p0 + tid; p < p1; p += NT) {
@@ -286,6 +296,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
 #else
             const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
 #endif
+#ifndef PIC_EXP_NOPUSH   // timing experiment only: no gather, no Boris
             const double ex = trilinear(eb + 0 * NE, hx + EPX * ty + EPY * tz, EPX, EPY, wx.fh, wy.f0, wz.f0);
             const double ey = trilinear(eb + 1 * NE, tx + EPX * hy + EPY * tz, EPX, EPY, wx.f0, wy.fh, wz.f0);
             const double ez = trilinear(eb + 2 * NE, tx + EPX * ty + EPY * hz, EPX, EPY, wx.f0, wy.f0, wz.fh);
@@ -298,6 +309,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
 #undef tz
 #endif
             boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
+#else
+            (void)hx; (void)hy; (void)hz;
+#endif
             const double ig = rsqrt_ge1(1.0 + (ux * ux + uy * uy + uz * uz));
             const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
             // move endpoints in start-cell coordinates (a = fractional parts, exact)
@@ -306,12 +320,17 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
             const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
             u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+#ifdef PIC_EXP_NOSTORE
+            if (xn == 1.2345e300) out.x[p] = yn + zn;
+            else
+#endif
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
                                kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, copy_id != 0, err);
             else
                 store_particle<kGeneral>(g, sp, out, in.id, p, x, y, z, ux, uy, uz, copy_id != 0, err);
             if (ok) {
+#ifndef PIC_EXP_NODEP   // timing experiment only: no deposit
                 const int jbase = tx + JPX * ty + JPY * tz;
                 double ex_, ey_, ez_, r1[3], r2[3];
                 int cx, cy, cz;
@@ -332,6 +351,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                                              r2[2], kx, ky, kz, scale);
                     }
                 }
+#endif
             } else {
                 atomicOr(err, (isfinite(xn) && isfinite(yn) && isfinite(zn)) ? kErrDisplacement
                                                                               : kErrNonFinite);
@@ -367,6 +387,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     __syncthreads();
     // flush the fixed-point tile to the fp64 global J: one thread per (comp, z, y) row
     const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
+#ifdef PIC_EXP_NOFLUSH
+    if (P0 < 0)
+#endif
     for (int row = tid; row < 3 * TJ * TJ; row += NT) {
         const int comp = row / (TJ * TJ), c = (row / TJ) % TJ, b = row % TJ;
         const int base = comp * NJ + c * JPY + b * JPX;
@@ -393,6 +416,31 @@ __global__ void __launch_bounds__(256) k_u2max(ParticlesDev P, int64_t n, unsign
     if ((threadIdx.x & 31) == 0 && hi) atomicMax(out, hi);
 }
 
+// Once per step, before the particle kernels: the fixed-point scale of each
+// species' J tile from the previous step's speed bound, and the reset of this
+// step's bound.  Every contribution is bounded by |qw| c beta / (dx dy dz) *
+// 13/12 with beta <= 2 x the largest beta of the previous step (from its max
+// |u|^2); 2^F maps that bound to < 2^46 (see the fixed-point notes above).
+__global__ void k_step_prep(const unsigned *__restrict__ u2max_in, unsigned *__restrict__ u2max_out,
+                            double *__restrict__ scale, StepPrep p)
+{
+    const int s = threadIdx.x;
+    if (s >= p.n_species) return;
+    const double u2 = __longlong_as_double(((unsigned long long)u2max_in[s] << 32) | 0xffffffffull);
+    const double beta = fmax(1e-4, fmin(1.0, 2.0 * sqrt(u2 / (1.0 + u2))));
+    const double wmax = fabs(p.qw[s]) * p.c / p.dV * (13.0 / 12.0) * beta;
+    const int F = wmax > 0.0 ? min(1000, (int)floor(46.0 - log2(wmax))) : 1000;
+    scale[2 * s] = ldexp(1.0, F);
+    scale[2 * s + 1] = ldexp(1.0, -F);
+    u2max_out[s] = 0u;
+}
+
+void launch_step_prep(const unsigned *u2max_in, unsigned *u2max_out, double *scale, const StepPrep &p,
+                      cudaStream_t st)
+{
+    k_step_prep<<<1, 32, 0, st>>>(u2max_in, u2max_out, scale, p);
+}
+
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st)
 {
     cudaMemsetAsync(out, 0, sizeof(unsigned), st);
@@ -412,7 +460,8 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
     // splitting C2's 3200-particle supercells was measured slower (extra tile
     // loads and flushes outweigh the shorter last wave)
     const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + 8191) / 8192));
-    k_push_tile<S, H, kGeneral><<<nsc * split, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
+    const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)g.nsz);
+    k_push_tile<S, H, kGeneral><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
                                                                copy_id ? 1 : 0, split, err);
 }
 

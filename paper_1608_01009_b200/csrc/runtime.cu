@@ -55,6 +55,7 @@ struct Layout {
     size_t off_jrecv[2] = {};
     size_t off_rho = 0, off_rho_prev = 0, off_gauss0 = 0, off_acc = 0;   // diagnostics
     size_t off_laser = 0, off_step = 0;                                  // NEXT-1 open z
+    size_t off_scale = 0;                                                // J-tile scales
     size_t total = 0;
 };
 
@@ -178,6 +179,7 @@ Layout make_layout(const pic_config *c)
     L.off_acc = o; o = align_up(o + sizeof(double) * kAccSlots);
     L.off_laser = o; o = align_up(o + sizeof(double) * 8);
     L.off_step = o; o = align_up(o + sizeof(int64_t));
+    L.off_scale = o; o = align_up(o + sizeof(double) * 2 * PIC_MAX_SPECIES);
     L.total = o;
     return L;
 }
@@ -291,6 +293,7 @@ struct pic_ctx {
     // NEXT-1 open z: incident values of the current step and the device step counter
     double *laser = nullptr;
     int64_t *dev_step = nullptr;
+    double *tile_scale = nullptr;   // [species][2] fixed-point J-tile scale of the step
     double laser_par[6] = {0, 0, 0, 0, 0, 0};   // e0, omega, ramp, t0, pol_x, pol_y
     int64_t diag_last_step = -2;
     bool diag_have_g0 = false;
@@ -374,6 +377,10 @@ SpeciesDev species_dev(pic_ctx *ctx, int s, int jcur)
     sp.h = ctx->cfg.q[s] * g.dt / (2.0 * ctx->cfg.m[s] * g.c);
     sp.u2max_in = ctx->u2max[jcur] + s;
     sp.u2max_out = ctx->u2max[1 - jcur] + s;
+    sp.kx = sp.qw / (g.dt * g.dy * g.dz);
+    sp.ky = sp.qw / (g.dt * g.dx * g.dz);
+    sp.kz = sp.qw / (g.dt * g.dx * g.dy);
+    sp.scale = ctx->tile_scale + 2 * s;
     sp.mig = ctx->mig[s];
     return sp;
 }
@@ -477,8 +484,16 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
                                ctx->err, ctx->st, &launches);
     }
     StageMark m(ctx, 1, profile);
-    // u^2 bounds: this step reads parity jcur, writes parity 1 - jcur
-    cudaMemsetAsync(ctx->u2max[1 - jcur], 0, PIC_MAX_SPECIES * sizeof(unsigned), ctx->st);
+    // u^2 bounds: this step reads parity jcur (-> the J-tile scales), writes parity 1 - jcur
+    {
+        StepPrep p{};
+        p.n_species = (int)ctx->cfg.n_species;
+        for (int s = 0; s < p.n_species; ++s) p.qw[s] = ctx->cfg.q[s] * ctx->cfg.w[s];
+        p.c = g.c;
+        p.dV = g.dx * g.dy * g.dz;
+        launch_step_prep(ctx->u2max[jcur], ctx->u2max[1 - jcur], ctx->tile_scale, p, ctx->st);
+        ++launches;
+    }
     for (int s = 0; s < ctx->cfg.n_species; ++s) {
         if (!ctx->has_particles[s]) continue;
         const SpeciesDev sp = species_dev(ctx, s, jcur);
@@ -781,6 +796,7 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->acc = (double *)(ctx->ws + L.off_acc);
     ctx->laser = (double *)(ctx->ws + L.off_laser);
     ctx->dev_step = (int64_t *)(ctx->ws + L.off_step);
+    ctx->tile_scale = (double *)(ctx->ws + L.off_scale);
     ctx->L.g.laser = ctx->laser;
     ctx->laser_par[0] = cfg->laser_e0;
     ctx->laser_par[1] = cfg->laser_omega;

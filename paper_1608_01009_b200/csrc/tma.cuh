@@ -76,6 +76,13 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+// TMA-engine prefetch of [src, src + bytes) into L2 (no shared memory, no
+// completion tracking); src and bytes multiples of 16
+__device__ __forceinline__ void prefetch_l2_bulk(const void *src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
 // wait until at most one committed group is still in flight
