@@ -50,8 +50,7 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 void configure_tile_kernels();
 void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
                       const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                      const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
-                      cudaStream_t st);
+                      const SpeciesDev &sp, unsigned *err, int64_t mean_per_sc, cudaStream_t st);
 
 // ---- sort.cu : stable counting sort by (supercell, local cell) ----
 struct SortScratch {
@@ -64,6 +63,8 @@ struct SortScratch {
     uint32_t *block_sums;// [scan blocks]
 };
 size_t scan_block_count(int64_t nitems);
+// dst[0 .. *dev_n) = src[...] (the sorted ids into the state buffer)
+void launch_copy_ids(const uint64_t *src, uint64_t *dst, const int64_t *dev_n, int64_t cap, cudaStream_t st);
 // Sorts the *dev_n particle slots src -> dst (x,y,z,ux,uy,uz,id), dropping
 // dead slots (x == kDeadX); writes the supercell offsets sc_off[0..n_sc]
 // (int64) and the live count back to *dev_n.  Grids are sized for cap.

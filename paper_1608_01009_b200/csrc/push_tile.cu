@@ -183,7 +183,7 @@ template <int S, int H, bool kGeneral>
 __global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
 k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
             double *__restrict__ J, ParticlesDev in, ParticlesDev out,
-            const int64_t *__restrict__ sc_off, SpeciesDev sp, int copy_id, int split, unsigned *err)
+            const int64_t *__restrict__ sc_off, SpeciesDev sp, int split, unsigned *err)
 {
     using T = TileGeom<S, H>;
     constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = kTileThreads;
@@ -319,16 +319,16 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double byl = yn * g.inv_dy - (double)wy.i0;
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
             const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
-            u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+            u2loc = fmax(u2loc, u2);
 #ifdef PIC_EXP_NOSTORE
             if (xn == 1.2345e300) out.x[p] = yn + zn;
             else
 #endif
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
-                               kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, copy_id != 0, err);
+                               kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, false, err);
             else
-                store_particle<kGeneral>(g, sp, out, in.id, p, x, y, z, ux, uy, uz, copy_id != 0, err);
+                store_particle<kGeneral>(g, sp, out, in.id, p, x, y, z, ux, uy, uz, false, err);
             if (ok) {
 #ifndef PIC_EXP_NODEP   // timing experiment only: no deposit
                 const int jbase = tx + JPX * ty + JPY * tz;
@@ -365,7 +365,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             } else {
                 double xx = x, yy = y, zz = z;
                 push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
-                store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
+                store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
                 u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
             }
         }
@@ -381,7 +381,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         const int p = (int)fq[e];
         double xx = in.x[p], yy = in.y[p], zz = in.z[p], ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
         push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
-        store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, copy_id != 0, err);
+        store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
         u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
     }
     __syncthreads();
@@ -450,7 +450,7 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 template <int S, int H, bool kGeneral>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
                         const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                        const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
+                        const SpeciesDev &sp, unsigned *err, int64_t mean_per_sc,
                         cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
@@ -462,7 +462,7 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
     const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + 8191) / 8192));
     const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)g.nsz);
     k_push_tile<S, H, kGeneral><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
-                                                               copy_id ? 1 : 0, split, err);
+                                                               split, err);
 }
 
 bool tile_supported(int S) { return S == 2 || S == 4; }
@@ -490,18 +490,18 @@ void configure_tile_kernels()
 
 void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
                       const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                      const SpeciesDev &sp, bool copy_id, unsigned *err, int64_t mean_per_sc,
+                      const SpeciesDev &sp, unsigned *err, int64_t mean_per_sc,
                       cudaStream_t st)
 {
     const bool general = g.nranks > 1 || g.open_z;
     if (g.S == 4 && general)
-        launch_tile<4, 1, true>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+        launch_tile<4, 1, true>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
     else if (g.S == 4)
-        launch_tile<4, 1, false>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+        launch_tile<4, 1, false>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
     else if (g.S == 2 && general)
-        launch_tile<2, 1, true>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+        launch_tile<2, 1, true>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
     else if (g.S == 2)
-        launch_tile<2, 1, false>(map, g, EB, J, in, out, sc_off, sp, copy_id, err, mean_per_sc, st);
+        launch_tile<2, 1, false>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
 }
 
 }  // namespace pic

@@ -479,9 +479,14 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
     if (sort_now) {
         StageMark m(ctx, 0, profile);
         for (int s = 0; s < ctx->cfg.n_species; ++s)
-            if (ctx->has_particles[s])
+            if (ctx->has_particles[s]) {
                 sort_particles(g, ctx->A[s], ctx->B[s], ctx->dev_n + s, L.cap[s], ctx->sort, ctx->sc_off[s],
                                ctx->err, ctx->st, &launches);
+                if (ctx->use_tile) {   // the fused kernel never touches ids
+                    launch_copy_ids(ctx->B[s].id, ctx->A[s].id, ctx->dev_n + s, L.cap[s], ctx->st);
+                    ++launches;
+                }
+            }
     }
     StageMark m(ctx, 1, profile);
     // u^2 bounds: this step reads parity jcur (-> the J-tile scales), writes parity 1 - jcur
@@ -500,7 +505,7 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
         const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
         if (ctx->use_tile)
             launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s], sp,
-                             sort_now, ctx->err, L.cap[s] / std::max<int64_t>(1, L.n_sc), ctx->st);
+                             ctx->err, L.cap[s] / std::max<int64_t>(1, L.n_sc), ctx->st);
         else
             launch_push_tail(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], nullptr, ctx->dev_n + s, L.cap[s], sp,
                              sort_now, ctx->err, ctx->st);

@@ -292,6 +292,22 @@ k_gather(ParticlesDev src, ParticlesDev dst, const uint32_t *__restrict__ perm,
     }
 }
 
+// ids of the sorted order back into the state buffer (the particle kernel
+// reads the sorted B and writes A; ids do not change in a step)
+__global__ void __launch_bounds__(256)
+k_copy_ids(const uint64_t *__restrict__ src, uint64_t *__restrict__ dst, const int64_t *__restrict__ dev_n)
+{
+    const int64_t n = *dev_n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+void launch_copy_ids(const uint64_t *src, uint64_t *dst, const int64_t *dev_n, int64_t cap, cudaStream_t st)
+{
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 148 * 16));
+    k_copy_ids<<<blocks, 256, 0, st>>>(src, dst, dev_n);
+}
+
 // supercell offsets; the particle count becomes the number of live particles
 __global__ void k_sc_offsets(const uint32_t *__restrict__ start, int64_t n_sc, int cells_per_sc,
                              int64_t *__restrict__ sc_off, int64_t *__restrict__ dev_n)
