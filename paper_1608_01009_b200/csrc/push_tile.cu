@@ -312,7 +312,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
 #else
             (void)hx; (void)hy; (void)hz;
 #endif
-            const double ig = rsqrt_ge1(1.0 + (ux * ux + uy * uy + uz * uz));
+            const double u2 = ux * ux + uy * uy + uz * uz;
+            const double ig = rsqrt_ge1(1.0 + u2);
             const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
             // move endpoints in start-cell coordinates (a = fractional parts, exact)
             const double bxl = xn * g.inv_dx - (double)wx.i0;

@@ -5,6 +5,7 @@ wls=$1; shift
 mkdir -p gpurun_out
 cp paper_1608_01009_b200/libpic.so /tmp/cur.so
 for v in "$@"; do
+  if [ ! -f exp/libpic_$v.so ]; then echo "$v missing" | tee -a gpurun_out/ab.txt; continue; fi
   cp exp/libpic_$v.so paper_1608_01009_b200/libpic.so
   timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > /tmp/smoke_$v.log 2>&1 && sm=ok || sm=FAIL
   for w in $wls; do
