@@ -178,12 +178,13 @@ __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *
 }
 
 // kGeneral: slabs (nranks > 1) or an open z box (migration / absorption
-// in the final store); false for the single-domain periodic box
-template <int S, int H, bool kGeneral>
+// in the final store); false for the single-domain periodic box.
+// One CTA pushes every species of its supercell in turn, so the E/B tile
+// is loaded and the J tile zeroed and flushed once per supercell and step.
+template <int S, int H, bool kGeneral, int NSP>
 __global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
 k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
-            double *__restrict__ J, ParticlesDev in, ParticlesDev out,
-            const int64_t *__restrict__ sc_off, SpeciesDev sp, int split, unsigned *err)
+            double *__restrict__ J, const __grid_constant__ TileSpecies ts, int split, unsigned *err)
 {
     using T = TileGeom<S, H>;
     constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = kTileThreads;
@@ -206,13 +207,24 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     const int part = split == 1 ? 0 : (int)blockIdx.x % split;
     const int scy = blockIdx.y, scz = blockIdx.z;
     const int sc = scx + g.nsx * (scy + g.nsy * scz);
-    const int P0 = (int)sc_off[sc], P1 = (int)sc_off[sc + 1];
-    int p0 = P0, p1 = P1;
-    if (split > 1) {
-        p0 = P0 + (int)(((int64_t)(P1 - P0) * part) / split);
-        p1 = P0 + (int)(((int64_t)(P1 - P0) * (part + 1)) / split);
+    // this CTA's particle range of species s (a part of the supercell's when split)
+    auto range = [&](int s, int &a, int &b) {
+        const int P0 = (int)ts.sc_off[s][sc], P1 = (int)ts.sc_off[s][sc + 1];
+        a = P0;
+        b = P1;
+        if (split > 1) {
+            a = P0 + (int)(((int64_t)(P1 - P0) * part) / split);
+            b = P0 + (int)(((int64_t)(P1 - P0) * (part + 1)) / split);
+        }
+    };
+    int total = 0;
+#pragma unroll
+    for (int s = 0; s < NSP; ++s) {
+        int a, b;
+        range(s, a, b);
+        total += b - a;
     }
-    if (p0 == p1) return;   // empty (uniform per CTA)
+    if (total == 0) return;   // empty (uniform per CTA)
 
     // local-grid coordinates of the tile origin (same for the E/B and J tiles)
     const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
@@ -221,21 +233,44 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     if (tid == 0) {
         mbar_init(bar_eb, 1);
         fence_mbar_init();
-#ifndef PIC_EXP_NOTMA
         mbar_arrive_expect_tx(bar_eb, 6 * NE * sizeof(double));
         tma_load_4d(eb, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, bar_eb);
-#endif
     }
-#ifdef PIC_PF_L2
-    if (tid < 6) {
-        // the CTA's whole particle range into L2 up front: the per-thread
-        // staging below then waits on L2, not HBM, latency
-        const double *arr = tid == 0 ? in.x : tid == 1 ? in.y : tid == 2 ? in.z : tid == 3 ? in.ux : tid == 4 ? in.uy : in.uz;
-        const uintptr_t a0 = (uintptr_t)(arr + p0) & ~(uintptr_t)15;
-        const uintptr_t a1 = ((uintptr_t)(arr + p1) + 15) & ~(uintptr_t)15;
-        prefetch_l2_bulk((const void *)a0, (unsigned)(a1 - a0));
+    {   // zero the fixed-point J tile (16-byte stores)
+        uint4 *j4 = (uint4 *)jt;
+        for (int t = tid; t < (9 * NJ) / 4; t += NT) j4[t] = make_uint4(0u, 0u, 0u, 0u);
+        for (int t = (9 * NJ) / 4 * 4 + tid; t < 9 * NJ; t += NT) jt[t] = 0u;
     }
-#endif
+    if (tid == 0) {
+        *qcount = 0u;
+        *fqcount = 0u;
+    }
+
+    const double cdt = g.c * g.dt;
+    // fixed-point scale 2^F of this step (k_step_prep): the smallest over the
+    // species, so every species' contributions stay inside the range
+    double scale = ts.sp[0].scale[0], inv_scale = ts.sp[0].scale[1];
+#pragma unroll
+    for (int s = 1; s < NSP; ++s)
+        if (ts.sp[s].scale[0] < scale) {
+            scale = ts.sp[s].scale[0];
+            inv_scale = ts.sp[s].scale[1];
+        }
+    const bool tile_ok = total <= kMaxTileParticles;   // else the counters could overflow
+    __syncthreads();
+    mbar_wait(bar_eb, 0);
+
+    // NSP is a template parameter so every species' pointers and constants
+    // stay kernel-parameter (constant bank) operands instead of registers
+#pragma unroll
+    for (int s = 0; s < NSP; ++s) {
+    int p0, p1;
+    range(s, p0, p1);
+    if (p0 == p1) continue;   // uniform per CTA
+    const ParticlesDev &in = ts.in[s], &out = ts.out[s];
+    const SpeciesDev &sp = ts.sp[s];
+    const double kx = sp.kx, ky = sp.ky, kz = sp.kz;   // q w / (dt dA), host
+    double u2loc = 0.0;   // this thread's max |u|^2 after the push
     auto stage = [&](int p, int st) {   // this thread's particle p -> its staging slot
         double *d = pbuf + st * 6 * NT + tid;
         cp_async8(d + 0 * NT, in.x + p);
@@ -247,29 +282,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     };
     if (p0 + tid < p1) stage(p0 + tid, 0);
     cp_async_commit();
-    {   // zero the fixed-point J tile (16-byte stores)
-        uint4 *j4 = (uint4 *)jt;
-#ifndef PIC_EXP_NOZERO
-        for (int t = tid; t < (9 * NJ) / 4; t += NT) j4[t] = make_uint4(0u, 0u, 0u, 0u);
-#endif
-        for (int t = (9 * NJ) / 4 * 4 + tid; t < 9 * NJ; t += NT) jt[t] = 0u;
-    }
-    if (tid == 0) {
-        *qcount = 0u;
-        *fqcount = 0u;
-    }
-
-    const double kx = sp.kx, ky = sp.ky, kz = sp.kz;   // q w / (dt dA), host
-    const double cdt = g.c * g.dt;
-    // fixed-point scale 2^F of this step (k_step_prep, once per launch)
-    const double scale = sp.scale[0], inv_scale = sp.scale[1];
-    double u2loc = 0.0;   // this thread's max |u|^2 after the push
-    const bool tile_ok = (p1 - p0) <= kMaxTileParticles;   // else the counters could overflow
-    __syncthreads();
-#ifndef PIC_EXP_NOTMA
-    mbar_wait(bar_eb, 0);
-#endif
-
     int st = 0;
     for (int p = p0 + tid; p < p1; p += NT) {
         if (p + NT < p1) stage(p + NT, st ^ 1);   // prefetch the next particle
@@ -321,10 +333,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
             const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
             u2loc = fmax(u2loc, u2);
-#ifdef PIC_EXP_NOSTORE
-            if (xn == 1.2345e300) out.x[p] = yn + zn;
-            else
-#endif
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
                                kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, false, err);
@@ -385,12 +393,19 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
         u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
     }
+    {
+        const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc) >> 32));
+        if (lane == 0 && hi) atomicMax(sp.u2max_out, hi);
+    }
+    __syncthreads();   // queues drained: reset them for the next species
+    if (tid == 0) {
+        *qcount = 0u;
+        *fqcount = 0u;
+    }
     __syncthreads();
+    }   // species
     // flush the fixed-point tile to the fp64 global J: one thread per (comp, z, y) row
     const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
-#ifdef PIC_EXP_NOFLUSH
-    if (P0 < 0)
-#endif
     for (int row = tid; row < 3 * TJ * TJ; row += NT) {
         const int comp = row / (TJ * TJ), c = (row / TJ) % TJ, b = row % TJ;
         const int base = comp * NJ + c * JPY + b * JPX;
@@ -401,10 +416,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                                  (long long)jt[3 * NJ + base + a] * 65536LL + (long long)jt[base + a];
             if (fx != 0) atomicAdd(Jrow + a, (double)fx * inv_scale);
         }
-    }
-    {
-        const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc) >> 32));
-        if (lane == 0 && hi) atomicMax(sp.u2max_out, hi);
     }
 }
 
@@ -450,20 +461,21 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 
 template <int S, int H, bool kGeneral>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
-                        const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                        const SpeciesDev &sp, unsigned *err, int64_t mean_per_sc,
-                        cudaStream_t st)
+                        const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
-    const int nsc = g.nsx * g.nsy * g.nsz;
     // one CTA per supercell (empty ones exit at once); only very dense
     // supercells (> 8192 particles expected) are split over several CTAs --
     // splitting C2's 3200-particle supercells was measured slower (extra tile
     // loads and flushes outweigh the shorter last wave)
     const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + 8191) / 8192));
     const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)g.nsz);
-    k_push_tile<S, H, kGeneral><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, in, out, sc_off, sp,
-                                                               split, err);
+    switch (ts.n) {
+    case 1: k_push_tile<S, H, kGeneral, 1><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
+    case 2: k_push_tile<S, H, kGeneral, 2><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
+    case 3: k_push_tile<S, H, kGeneral, 3><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
+    default: k_push_tile<S, H, kGeneral, 4><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
+    }
 }
 
 bool tile_supported(int S) { return S == 2 || S == 4; }
@@ -477,32 +489,37 @@ void tile_box(int S, int box[4])
     box[3] = 6;
 }
 
+template <int S, bool G>
+static void set_smem()
+{
+    const int b = (int)TileGeom<S, 1>::smem_bytes;
+    cudaFuncSetAttribute(k_push_tile<S, 1, G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_push_tile<S, 1, G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_push_tile<S, 1, G, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_push_tile<S, 1, G, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
 void configure_tile_kernels()
 {
-    cudaFuncSetAttribute(k_push_tile<4, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TileGeom<4, 1>::smem_bytes);
-    cudaFuncSetAttribute(k_push_tile<2, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TileGeom<2, 1>::smem_bytes);
-    cudaFuncSetAttribute(k_push_tile<4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TileGeom<4, 1>::smem_bytes);
-    cudaFuncSetAttribute(k_push_tile<2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TileGeom<2, 1>::smem_bytes);
+    set_smem<4, false>();
+    set_smem<4, true>();
+    set_smem<2, false>();
+    set_smem<2, true>();
 }
 
 void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
-                      const ParticlesDev &in, const ParticlesDev &out, const int64_t *sc_off,
-                      const SpeciesDev &sp, unsigned *err, int64_t mean_per_sc,
-                      cudaStream_t st)
+                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st)
 {
+    if (ts.n == 0) return;
     const bool general = g.nranks > 1 || g.open_z;
     if (g.S == 4 && general)
-        launch_tile<4, 1, true>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
+        launch_tile<4, 1, true>(map, g, EB, J, ts, err, mean_per_sc, st);
     else if (g.S == 4)
-        launch_tile<4, 1, false>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
+        launch_tile<4, 1, false>(map, g, EB, J, ts, err, mean_per_sc, st);
     else if (g.S == 2 && general)
-        launch_tile<2, 1, true>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
+        launch_tile<2, 1, true>(map, g, EB, J, ts, err, mean_per_sc, st);
     else if (g.S == 2)
-        launch_tile<2, 1, false>(map, g, EB, J, in, out, sc_off, sp, err, mean_per_sc, st);
+        launch_tile<2, 1, false>(map, g, EB, J, ts, err, mean_per_sc, st);
 }
 
 }  // namespace pic

@@ -499,18 +499,37 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
         launch_step_prep(ctx->u2max[jcur], ctx->u2max[1 - jcur], ctx->tile_scale, p, ctx->st);
         ++launches;
     }
+    if (ctx->use_tile) {
+        // one fused launch for every species: the E/B tile, the J tile and its
+        // flush are shared by the species of a supercell
+        TileSpecies ts{};
+        int64_t cap_total = 0;
+        for (int s = 0; s < ctx->cfg.n_species; ++s) {
+            if (!ctx->has_particles[s]) continue;
+            ts.in[ts.n] = sort_now ? ctx->B[s] : ctx->A[s];
+            ts.out[ts.n] = ctx->A[s];
+            ts.sc_off[ts.n] = ctx->sc_off[s];
+            ts.sp[ts.n] = species_dev(ctx, s, jcur);
+            cap_total += L.cap[s];
+            ++ts.n;
+        }
+        if (ts.n > 0) {
+            launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], ts, ctx->err,
+                             cap_total / std::max<int64_t>(1, L.n_sc), ctx->st);
+            ++launches;
+            if (profile) ctx->particle_launches++;
+        }
+    }
     for (int s = 0; s < ctx->cfg.n_species; ++s) {
         if (!ctx->has_particles[s]) continue;
         const SpeciesDev sp = species_dev(ctx, s, jcur);
-        const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
-        if (ctx->use_tile)
-            launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], in, ctx->A[s], ctx->sc_off[s], sp,
-                             ctx->err, L.cap[s] / std::max<int64_t>(1, L.n_sc), ctx->st);
-        else
+        if (!ctx->use_tile) {
+            const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
             launch_push_tail(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], nullptr, ctx->dev_n + s, L.cap[s], sp,
                              sort_now, ctx->err, ctx->st);
-        ++launches;
-        if (profile) ctx->particle_launches++;
+            ++launches;
+            if (profile) ctx->particle_launches++;
+        }
         if (ctx->slabs) {
             if (ctx->use_tile) {   // particles received since the last sort (none right after it)
                 if (!sort_now) {
