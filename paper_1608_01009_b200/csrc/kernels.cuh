@@ -57,6 +57,8 @@ struct TileSpecies {
     SpeciesDev sp[kTileMaxSpecies];
     int n;
 };
+// number of supercells holding particles of the species of ts (synchronises st)
+int64_t count_occupied(const GridDev &g, const TileSpecies &ts, unsigned *scratch, cudaStream_t st);
 // mean_per_sc: particles per supercell over all species (splits very dense supercells)
 void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
                       const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st);

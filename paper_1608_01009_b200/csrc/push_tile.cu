@@ -478,6 +478,28 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
     }
 }
 
+// supercells holding particles of any species of ts (set-up time only)
+__global__ void __launch_bounds__(256) k_count_occupied(TileSpecies ts, int n_sc, unsigned *count)
+{
+    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+    bool occ = false;
+    if (sc < n_sc)
+        for (int s = 0; s < ts.n; ++s) occ |= ts.sc_off[s][sc + 1] > ts.sc_off[s][sc];
+    const unsigned m = __ballot_sync(0xffffffffu, occ);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned)__popc(m));
+}
+
+int64_t count_occupied(const GridDev &g, const TileSpecies &ts, unsigned *scratch, cudaStream_t st)
+{
+    const int n_sc = g.nsx * g.nsy * g.nsz;
+    unsigned h = 0;
+    cudaMemsetAsync(scratch, 0, sizeof(unsigned), st);
+    if (ts.n > 0) k_count_occupied<<<(n_sc + 255) / 256, 256, 0, st>>>(ts, n_sc, scratch);
+    cudaMemcpyAsync(&h, scratch, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return (int64_t)h;
+}
+
 bool tile_supported(int S) { return S == 2 || S == 4; }
 
 void tile_box(int S, int box[4])
