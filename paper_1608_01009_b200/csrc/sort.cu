@@ -49,24 +49,39 @@ k_sort_key(GridDev g, ParticlesDev src, const int64_t *__restrict__ dev_n, uint3
            uint32_t *__restrict__ slot, uint32_t *__restrict__ count, unsigned *err)
 {
     const int64_t n = *dev_n;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const double x = src.x[p], y = src.y[p], z = src.z[p];
-        if (x == kDeadX) {   // slot left by a particle that migrated: dropped here
-            key[p] = kDeadKey;
-            continue;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int S = g.S;
+    // kU particles per thread and iteration: their loads and their (returning)
+    // counter atomics are in flight together instead of one latency each
+    constexpr int kU = 4;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += kU * stride) {
+        uint32_t k[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t p = p0 + u * stride;
+            k[u] = kDeadKey;
+            if (p >= n) continue;
+            const double x = src.x[p], y = src.y[p], z = src.z[p];
+            if (x == kDeadX) continue;   // slot left by a particle that migrated: dropped here
+            if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= g.zlo && z < g.zhi))
+                atomicOr(err, isfinite(x) && isfinite(y) && isfinite(z) ? kErrRange : kErrNonFinite);
+            const int cx = cell_of(x, g.dx, g.nx, 0);
+            const int cy = cell_of(y, g.dy, g.ny, 0);
+            const int cz = cell_of(z, g.dz, g.nz, g.k0);
+            const uint32_t sc = (uint32_t)((cx / S) + g.nsx * ((cy / S) + g.nsy * (cz / S)));
+            const uint32_t loc = (uint32_t)((cx % S) + S * ((cy % S) + S * (cz % S)));
+            k[u] = sc * (uint32_t)(S * S * S) + loc;
         }
-        if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= g.zlo && z < g.zhi))
-            atomicOr(err, isfinite(x) && isfinite(y) && isfinite(z) ? kErrRange : kErrNonFinite);
-        const int cx = cell_of(x, g.dx, g.nx, 0);
-        const int cy = cell_of(y, g.dy, g.ny, 0);
-        const int cz = cell_of(z, g.dz, g.nz, g.k0);
-        const int S = g.S;
-        const uint32_t sc = (uint32_t)((cx / S) + g.nsx * ((cy / S) + g.nsy * (cz / S)));
-        const uint32_t loc = (uint32_t)((cx % S) + S * ((cy % S) + S * (cz % S)));
-        const uint32_t k = sc * (uint32_t)(S * S * S) + loc;
-        key[p] = k;
-        slot[p] = atomicAdd(count + k, 1u);
+        uint32_t sl[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) sl[u] = k[u] != kDeadKey ? atomicAdd(count + k[u], 1u) : 0u;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t p = p0 + u * stride;
+            if (p >= n) continue;
+            key[p] = k[u];
+            slot[p] = sl[u];
+        }
     }
 }
 
@@ -167,7 +182,54 @@ k_scatter(const uint32_t *__restrict__ key, const uint32_t *__restrict__ slot,
     }
 }
 
+// bitonic sort of 64 keys held as 2 per lane (k0 = element lane, k1 =
+// element 32 + lane), ascending; padding keys are 0xffffffff
+__device__ __forceinline__ void warp_sort64(uint32_t &k0, uint32_t &k1)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride == 32) {   // partners are k0 / k1 of the same lane
+                const uint32_t lo = min(k0, k1), hi = max(k0, k1);
+                // element index i = lane (k0) or 32 + lane (k1); direction from i & size
+                const bool up0 = ((lane & size) == 0);
+                k0 = up0 ? lo : hi;
+                k1 = up0 ? hi : lo;
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t &k = h ? k1 : k0;
+                    const int i = lane + 32 * h;
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, k, stride);
+                    const bool lower = (i & stride) == 0;          // this element is the pair's first
+                    const bool asc = (i & size) == 0;               // this pair sorts ascending
+                    k = (lower == asc) ? min(k, o) : max(k, o);
+                }
+            }
+        }
+    }
+}
+
+// bitonic sort of 32 keys, one per lane, ascending
+__device__ __forceinline__ uint32_t warp_sort32(uint32_t k)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, k, stride);
+            const bool lower = (lane & stride) == 0, asc = (lane & size) == 0;
+            k = (lower == asc) ? min(k, o) : max(k, o);
+        }
+    }
+    return k;
+}
+
 // one warp per bucket: perm[start + rank(v)] = v with rank = #{u < v}
+// (the input indices of the bucket in ascending order = its stable order)
 __global__ void __launch_bounds__(256)
 k_bucket_order(const uint32_t *__restrict__ start, int64_t nbuckets,
                const uint32_t *__restrict__ perm_tmp, uint32_t *__restrict__ perm)
@@ -180,6 +242,20 @@ k_bucket_order(const uint32_t *__restrict__ start, int64_t nbuckets,
     if (m == 0) return;
     if (m == 1) {
         if (lane == 0) perm[s] = perm_tmp[s];
+        return;
+    }
+    if (m <= 32) {   // the common cases: a bitonic sort in registers
+        uint32_t k = (uint32_t)lane < m ? perm_tmp[s + lane] : 0xffffffffu;
+        k = warp_sort32(k);
+        if ((uint32_t)lane < m) perm[s + lane] = k;
+        return;
+    }
+    if (m <= 64) {
+        uint32_t k0 = (uint32_t)lane < m ? perm_tmp[s + lane] : 0xffffffffu;
+        uint32_t k1 = (uint32_t)lane + 32 < m ? perm_tmp[s + 32 + lane] : 0xffffffffu;
+        warp_sort64(k0, k1);
+        if ((uint32_t)lane < m) perm[s + lane] = k0;
+        if ((uint32_t)lane + 32 < m) perm[s + 32 + lane] = k1;
         return;
     }
     for (uint32_t i0 = 0; i0 < m; i0 += 32) {
