@@ -335,19 +335,20 @@ def run_ours(args, wl, rank, world, local):
     del psim
     torch.cuda.empty_cache()
     ppc_cells = occupied_cells(wl, slab[0], slab[1])
-    alg_bytes_total = sum(p.shape[1] for p, _ in parts) * 96.0 + len(parts) * ppc_cells * 72.0
     n_launch = max(st["particle_launches"], 1)
+    per_step_launches = n_launch / args.steps   # species per launch: 1, or all of them (sparse box)
+    # algorithmic bytes of one launch: x, u read + write (96 B) of its particles,
+    # E/B tile gather (48 B) + J write (24 B) of the occupied cells once per launch
+    per_launch_bytes = (n_local * 96.0) / per_step_launches + ppc_cells * 72.0
+    alg_bytes_total = per_launch_bytes * per_step_launches
     per_launch_ms = st["particle"] / n_launch
-    per_launch_bytes = alg_bytes_total / len(parts)
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     peak, peak_src = load_peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_particle_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp):   # ncu dram read + write of one launch, per workload
         try:
-            d = json.load(open(tp))
-            if d.get("workload") == wl.name:
-                traffic = d.get("bytes_per_launch")
+            traffic = json.load(open(tp)).get(wl.name, {}).get("bytes_per_launch")
         except Exception:
             pass
     step_ms_prof = (st["sort"] + st["particle"] + st["field"] + st["exchange"]) / args.steps
@@ -356,7 +357,7 @@ def run_ours(args, wl, rank, world, local):
     e2e = None
     if not args.no_e2e:
         pinned = [pinned_copy(P, ids) for P, ids in parts]
-        outs = [(np.empty_like(P), np.empty_like(ids)) for P, ids in parts]
+        outs = [pinned_copy(np.empty_like(P), np.empty_like(ids)) for P, ids in parts]   # pinned results
         esim = new_sim()
         load(esim, [(Pn, In) for _, _, Pn, In in pinned])
         esim.step(args.warmup)
@@ -367,7 +368,7 @@ def run_ours(args, wl, rank, world, local):
             esim.set_particles(s, Pn, In)
         esim.step(args.steps)
         for s in range(len(parts)):
-            esim.get_particles(s, out=outs[s])
+            esim.get_particles(s, out=outs[s][2:])
         torch.cuda.synchronize()
         barrier()
         te = reduce_max_over_ranks(time.perf_counter() - t0)

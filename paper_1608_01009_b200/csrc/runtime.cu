@@ -890,11 +890,15 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
     if (n < 0 || (n > 0 && !(x && y && z && ux && uy && uz && id)))
         return fail(ctx, PIC_EINVAL, "bad particle arrays");
     const GridDev &g = ctx->L.g;
-    for (int64_t p = 0; p < n; ++p) {
-        if (!(x[p] >= 0.0 && x[p] < g.Lx && y[p] >= 0.0 && y[p] < g.Ly && z[p] >= 0.0 && z[p] < g.zmax))
-            return fail(ctx, PIC_EINVAL, g.open_z ? "particle position outside [0, Lx) x [0, Ly) x [0, (nz-1) dz)"
-                                                  : "particle position outside [0, L)");
-    }
+    const char *outside = g.open_z ? "particle position outside [0, Lx) x [0, Ly) x [0, (nz-1) dz)"
+                                   : "particle position outside [0, L)";
+    // slabs select their particles on the host, so they check there; a single
+    // domain leaves the check to the device (the sort's key pass flags any
+    // position outside the box), which keeps the host out of the upload path
+    if (ctx->slabs)
+        for (int64_t p = 0; p < n; ++p)
+            if (!(x[p] >= 0.0 && x[p] < g.Lx && y[p] >= 0.0 && y[p] < g.Ly && z[p] >= 0.0 && z[p] < g.zmax))
+                return fail(ctx, PIC_EINVAL, outside);
     const double *src[6] = {x, y, z, ux, uy, uz};
     std::vector<double> sel[6];
     std::vector<uint64_t> sel_id;
@@ -911,6 +915,7 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
         id = sel_id.data();
     }
     if (m > ctx->L.cap[species]) return fail(ctx, PIC_ECAPACITY, "n exceeds capacity");
+    if (!ctx->slabs) PIC_CUDA(ctx, cudaMemsetAsync(ctx->err, 0, sizeof(unsigned), ctx->st));   // fresh check
     const ParticlesDev &Bs = ctx->B[species];
     double *dst[6] = {Bs.x, Bs.y, Bs.z, Bs.ux, Bs.uy, Bs.uz};
     for (int c = 0; c < 6 && m > 0; ++c)
@@ -924,6 +929,23 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
                    ctx->sc_off[species], ctx->err, ctx->st, &launches);
     launch_u2max(ctx->A[species], m, ctx->u2max[ctx->jcur] + species, ctx->st);
     ctx->launches += launches + 1;
+    if (!ctx->slabs) {   // the device-side range check of the key pass
+        unsigned h = 0;
+        PIC_CUDA(ctx, cudaMemcpyAsync(&h, ctx->err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->st));
+        PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        if (h & (kErrRange | kErrNonFinite)) {   // reject: the species is left empty
+            const int64_t zero = 0;
+            PIC_CUDA(ctx, cudaMemsetAsync(ctx->err, 0, sizeof(unsigned), ctx->st));
+            PIC_CUDA(ctx, cudaMemcpyAsync(ctx->dev_n + species, &zero, sizeof(int64_t), cudaMemcpyHostToDevice,
+                                          ctx->st));
+            PIC_CUDA(ctx, cudaMemsetAsync(ctx->sc_off[species], 0, sizeof(int64_t) * (size_t)(ctx->L.n_sc + 1),
+                                          ctx->st));
+            PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            ctx->has_particles[species] = false;
+            destroy_graphs(ctx);
+            return fail(ctx, PIC_EINVAL, outside);
+        }
+    }
     if (ctx->use_tile) {
         // merge the species into one launch when fewer than half of the
         // supercells hold particles (decided on every pic_set_particles)

@@ -63,7 +63,7 @@ k_sort_key(GridDev g, ParticlesDev src, const int64_t *__restrict__ dev_n, uint3
             if (p >= n) continue;
             const double x = src.x[p], y = src.y[p], z = src.z[p];
             if (x == kDeadX) continue;   // slot left by a particle that migrated: dropped here
-            if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= g.zlo && z < g.zhi))
+            if (!(x >= 0.0 && x < g.Lx && y >= 0.0 && y < g.Ly && z >= g.zlo && z < fmin(g.zhi, g.zmax)))
                 atomicOr(err, isfinite(x) && isfinite(y) && isfinite(z) ? kErrRange : kErrNonFinite);
             const int cx = cell_of(x, g.dx, g.nx, 0);
             const int cy = cell_of(y, g.dy, g.ny, 0);

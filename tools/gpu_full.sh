@@ -15,3 +15,4 @@ timeout 900 python bench.py --workload C5_1g --steps 100 --warmup 5 > gpurun_out
 timeout 900 python bench.py --workload FROZEN --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/bench_frozen_$tag.json 2> gpurun_out/bench_frozen_$tag.err; echo "FROZEN rc=$?"
 python tools/run_steps.py C3 8 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_push_tile -s 3 -c 1 -o gpurun_out/prof_C3_$tag python tools/run_steps.py C3 8 > gpurun_out/ncu_C3_$tag.log 2>&1; echo "ncu C3 rc=$?"
 python tools/run_steps.py C2 25 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_push_tile -s 3 -c 1 -o gpurun_out/prof_C2_$tag python tools/run_steps.py C2 25 > gpurun_out/ncu_C2_$tag.log 2>&1; echo "ncu C2 rc=$?"
+timeout 1200 python bench.py --workload C4 --steps 40 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_C4_$tag.json 2> gpurun_out/bench_C4_$tag.err; echo "C4 rc=$?"
