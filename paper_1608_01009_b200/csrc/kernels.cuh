@@ -74,6 +74,10 @@ struct SortScratch {
     uint32_t *block_sums;// [scan blocks]
 };
 size_t scan_block_count(int64_t nitems);
+// stable copy of the live slots [0, n) of src (x != kDeadX) to dst[0, live);
+// returns live (synchronises st).  bsums: scan_block_count(n + 1) entries
+int64_t compact_live(const ParticlesDev &src, const ParticlesDev &dst, int64_t n, const SortScratch &s,
+                     uint32_t *bsums, cudaStream_t st);
 // dst[0 .. *dev_n) = src[...] (the sorted ids into the state buffer)
 void launch_copy_ids(const uint64_t *src, uint64_t *dst, const int64_t *dev_n, int64_t cap, cudaStream_t st);
 // Sorts the *dev_n particle slots src -> dst (x,y,z,ux,uy,uz,id), dropping

@@ -50,7 +50,7 @@ struct Layout {
     int64_t mig = 0;   // migration capacity (per species and direction), 0 on one rank
     size_t off_eb = 0, off_j[2] = {}, off_sp[PIC_MAX_SPECIES][2] = {}, off_scoff[PIC_MAX_SPECIES] = {};
     size_t off_key = 0, off_slot = 0, off_perm_tmp = 0, off_perm = 0, off_count = 0, off_start = 0,
-           off_bsums = 0, off_err = 0, off_stat = 0, off_n = 0;
+           off_bsums = 0, off_bsums2 = 0, off_err = 0, off_stat = 0, off_n = 0;
     size_t off_msend[PIC_MAX_SPECIES][2] = {}, off_mrecv[PIC_MAX_SPECIES][2] = {}, off_mcnt = 0;
     size_t off_jrecv[2] = {};
     size_t off_rho = 0, off_rho_prev = 0, off_gauss0 = 0, off_acc = 0;   // diagnostics
@@ -170,6 +170,7 @@ Layout make_layout(const pic_config *c)
     L.off_count = o; o = align_up(o + 4 * (size_t)(L.ncells + 1));
     L.off_start = o; o = align_up(o + 4 * (size_t)(L.ncells + 1));
     L.off_bsums = o; o = align_up(o + 4 * scan_block_count(L.ncells + 1));
+    L.off_bsums2 = o; o = align_up(o + 4 * scan_block_count(L.cap_max + 1));   // compact_live
     L.off_err = o; o = align_up(o + 64);
     L.off_stat = o; o = align_up(o + 2 * PIC_MAX_SPECIES * sizeof(unsigned));
     L.off_n = o; o = align_up(o + PIC_MAX_SPECIES * sizeof(int64_t));
@@ -1037,30 +1038,22 @@ int pic_get_particles(pic_ctx *ctx, int species, int64_t *n_inout, double *x, do
         PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         return PIC_OK;
     }
-    // slabs / open z: skip dead slots (x == -1) left by migration or absorption
-    std::vector<double> buf[6];
-    std::vector<uint64_t> ibuf((size_t)slots);
-    for (int c = 0; c < 6; ++c) {
-        buf[c].resize((size_t)slots);
-        if (slots > 0)
-            PIC_CUDA(ctx, cudaMemcpyAsync(buf[c].data(), src[c], sizeof(double) * (size_t)slots,
-                                          cudaMemcpyDeviceToHost, ctx->st));
-    }
-    if (slots > 0)
-        PIC_CUDA(ctx, cudaMemcpyAsync(ibuf.data(), A.id, sizeof(uint64_t) * (size_t)slots, cudaMemcpyDeviceToHost, ctx->st));
-    PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-    int64_t live = 0;
-    for (int64_t p = 0; p < slots; ++p) live += buf[0][(size_t)p] >= 0.0;
+    // slabs / open z: skip the dead slots (x == -1) left by migration or
+    // absorption -- a stable device compaction into B (free between steps)
+    const ParticlesDev &Bs = ctx->B[species];
+    const int64_t live = compact_live(A, Bs, slots, ctx->sort, (uint32_t *)(ctx->ws + ctx->L.off_bsums2), ctx->st);
+    ctx->launches += 5;
+    PIC_CUDA(ctx, cudaGetLastError());
     *n_inout = live;
     if (capacity < live) return fail(ctx, PIC_ECAPACITY, "output arrays too small");
-    int64_t k = 0;
-    for (int64_t p = 0; p < slots; ++p) {
-        if (buf[0][(size_t)p] < 0.0) continue;
-        for (int c = 0; c < 6; ++c)
-            if (dst[c]) dst[c][k] = buf[c][(size_t)p];
-        if (id) id[k] = ibuf[(size_t)p];
-        ++k;
-    }
+    const double *bsrc[6] = {Bs.x, Bs.y, Bs.z, Bs.ux, Bs.uy, Bs.uz};
+    for (int c = 0; c < 6 && live > 0; ++c)
+        if (dst[c])
+            PIC_CUDA(ctx, cudaMemcpyAsync(dst[c], bsrc[c], sizeof(double) * (size_t)live, cudaMemcpyDeviceToHost,
+                                          ctx->st));
+    if (id && live > 0)
+        PIC_CUDA(ctx, cudaMemcpyAsync(id, Bs.id, sizeof(uint64_t) * (size_t)live, cudaMemcpyDeviceToHost, ctx->st));
+    PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return PIC_OK;
 }
 

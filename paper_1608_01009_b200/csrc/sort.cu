@@ -384,6 +384,48 @@ void launch_copy_ids(const uint64_t *src, uint64_t *dst, const int64_t *dev_n, i
     k_copy_ids<<<blocks, 256, 0, st>>>(src, dst, dev_n);
 }
 
+// ---- stable compaction of the live slots (pic_get_particles) ----
+__global__ void __launch_bounds__(256)
+k_live_flags(const double *__restrict__ x, int64_t n, uint32_t *__restrict__ flag)
+{
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= n; p += (int64_t)gridDim.x * blockDim.x)
+        flag[p] = (p < n && x[p] != kDeadX) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(256)
+k_compact(ParticlesDev src, ParticlesDev dst, int64_t n, const uint32_t *__restrict__ flag,
+          const uint32_t *__restrict__ off)
+{
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        if (!flag[p]) continue;
+        const uint32_t q = off[p];
+        dst.x[q] = src.x[p];
+        dst.y[q] = src.y[p];
+        dst.z[q] = src.z[p];
+        dst.ux[q] = src.ux[p];
+        dst.uy[q] = src.uy[p];
+        dst.uz[q] = src.uz[p];
+        dst.id[q] = src.id[p];
+    }
+}
+
+int64_t compact_live(const ParticlesDev &src, const ParticlesDev &dst, int64_t n, const SortScratch &s,
+                     uint32_t *bsums, cudaStream_t st)
+{
+    const int64_t nscan = n + 1;   // flag[n] = 0, so off[n] = live count
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nscan + 255) / 256, 148 * 32));
+    k_live_flags<<<blocks, 256, 0, st>>>(src.x, n, s.perm_tmp);
+    const int64_t nb = (int64_t)scan_block_count(nscan);
+    k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(s.perm_tmp, nscan, bsums);
+    k_scan_blocks<<<1, kScanThreads, 0, st>>>(bsums, nb);
+    k_scan_add<<<(unsigned)nb, kScanThreads, 0, st>>>(s.perm_tmp, nscan, bsums, s.perm);
+    k_compact<<<blocks, 256, 0, st>>>(src, dst, n, s.perm_tmp, s.perm);
+    uint32_t live = 0;
+    cudaMemcpyAsync(&live, s.perm + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return (int64_t)live;
+}
+
 // supercell offsets; the particle count becomes the number of live particles
 __global__ void k_sc_offsets(const uint32_t *__restrict__ start, int64_t n_sc, int cells_per_sc,
                              int64_t *__restrict__ sc_off, int64_t *__restrict__ dev_n)
