@@ -66,14 +66,25 @@ __device__ __forceinline__ double rcp_ge1(double d)
 
 __device__ __forceinline__ double rsqrt_ge1(double d)
 {
+    // MUFU seed (relative error < 2^-22.9) and two Newton steps in residual
+    // form, r' = r + r (1 - d r^2) / 2: 2^-45, then below the fp64 rounding
     double r;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-    const double hd = 0.5 * d;
-    r = r * fma(-hd * r, r, 1.5);
-    r = r * fma(-hd * r, r, 1.5);
-    // final correction step in residual form (y = r + r (1 - d r^2) / 2)
-    const double e = fma(-d * r, r, 1.0);
+    double e = fma(-d * r, r, 1.0);
+    r = fma(0.5 * r, e, r);
+    e = fma(-d * r, r, 1.0);
     return fma(0.5 * r, e, r);
+}
+
+// 1/d for a positive normal d (no special cases): MUFU seed + two Newton steps
+__device__ __forceinline__ double rcp_pos(double d)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
 }
 
 // Relativistic Boris rotation on u = gamma*beta (reading R1):
@@ -176,7 +187,7 @@ __device__ __forceinline__ bool vb_first_piece(double ax, double ay, double az, 
         double den = axis == 0 ? dxd : (axis == 1 ? dyd : dzd);
         if (cyq && axis < 1 && nyd * den < num * dyd) { axis = 1; num = nyd; den = dyd; }
         if (czq && axis < 2 && nzd * den < num * dzd) { axis = 2; num = nzd; den = dzd; }
-        const double t = num / den;
+        const double t = num * rcp_pos(den);   // den = |b_d - a_d| > 0 on a crossed axis
         ex = fma(t, bx - ax, ax);
         ey = fma(t, by - ay, ay);
         ez = fma(t, bz - az, az);
