@@ -96,7 +96,7 @@ template <class T>
 __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, int64_t gorigin,
                                             const GridDev &g, double p1x, double p1y, double p1z,
                                             double p2x, double p2y, double p2z, double kx,
-                                            double ky, double kz, double scale)
+                                            double ky, double kz, double scale, bool fits)
 {
     constexpr int PX = T::JPX, PY = T::JPY, NJ = T::NJ;
     const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
@@ -109,7 +109,7 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
     // |value| <= |f| (1 + 1/12): weights are products of numbers in [0,1], |c| <= 1/12.
     // f scaled by 2^F (exact): one fma per value then rounds f W 2^F + 1.5*2^52.
     const double fxs = fx * scale, fys = fy * scale, fzs = fz * scale;
-    if (!(fmax(fabs(fxs), fmax(fabs(fys), fabs(fzs))) * (13.0 / 12.0) < 140737488355328.0)) {   // 2^47
+    if (!fits) {   // values beyond the fixed-point range (rare): fp64 global atomics
         const int rem = jbase % PY, tx = rem % PX, ty = rem / PX, tz = jbase / PY;
         const int64_t X = g.X, XY = (int64_t)g.X * g.Y, cs = g.cs;
         double *b = J + gorigin + tx + X * ty + XY * tz;
@@ -156,20 +156,31 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
     add(2 * NJ + 1 + PX, fzs, fma(mx, my, czz));
 }
 
+// Do the tile values of a particle's path fit the fixed-point range?  Every
+// segment of the path has |D| <= |d| per axis (d = the whole displacement in
+// cell units), so |f W| <= |k d| (1 + 1/12) bounds all its values; a particle
+// that sped up by more than the 2x headroom of the scale since the last step
+// fails and deposits into the fp64 global J instead.
+__device__ __forceinline__ bool fits_tile(double dx, double dy, double dz, double kx, double ky, double kz,
+                                          double scale)
+{
+    return fmax(fabs(kx * dx), fmax(fabs(ky * dy), fabs(kz * dz))) * scale * (13.0 / 12.0) < 140737488355328.0;
+}
+
 // Deposits the rest of a split path (<= 2 more face crossings) starting in
 // the cell with J-tile index jb; a, b in that cell's coordinates.
 template <class T>
 __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *J, int64_t gorigin,
                                                   const GridDev &g, double a0, double a1,
                                                   double a2, double b0, double b1, double b2,
-                                                  double kx, double ky, double kz, double scale)
+                                                  double kx, double ky, double kz, double scale, bool fits)
 {
 #pragma unroll 1
     for (int it = 0; it < 3; ++it) {
         double e0, e1, e2, r1[3], r2[3];
         int ox, oy, oz;
         const bool more = vb_first_piece(a0, a1, a2, b0, b1, b2, e0, e1, e2, r1, r2, ox, oy, oz);
-        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale);
+        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale, fits);
         if (!more) break;
         jb += ox + T::JPX * oy + T::JPY * oz;
         a0 = r1[0]; a1 = r1[1]; a2 = r1[2];
@@ -331,7 +342,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double bxl = xn * g.inv_dx - (double)wx.i0;
             const double byl = yn * g.inv_dy - (double)wy.i0;
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
-            const bool ok = fabs(bxl - wx.f0) < 1.0 && fabs(byl - wy.f0) < 1.0 && fabs(bzl - wz.f0) < 1.0;
+            const double dxl = bxl - wx.f0, dyl = byl - wy.f0, dzl = bzl - wz.f0;
+            const bool ok = fabs(dxl) < 1.0 && fabs(dyl) < 1.0 && fabs(dzl) < 1.0;
             u2loc = fmax(u2loc, u2);
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
@@ -345,19 +357,22 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                 int cx, cy, cz;
                 const bool more =
                     vb_first_piece(wx.f0, wy.f0, wz.f0, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
-                deposit_seg<T>(jt, jbase, J, gorigin, g, wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx, ky, kz, scale);
+                const bool fits = fits_tile(dxl, dyl, dzl, kx, ky, kz, scale);
+                deposit_seg<T>(jt, jbase, J, gorigin, g, wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx, ky, kz, scale,
+                               fits);
                 if (more) {
                     // the rest of a face-crossing path is deposited after the particle
                     // loop, all queued paths together (keeps the loop convergent)
                     const int jrem = jbase + cx + JPX * cy + JPY * cz;
-                    const unsigned slot = atomicAdd(qcount, 1u);
+                    // only fitting paths are queued (the drain deposits into the tile)
+                    const unsigned slot = fits ? atomicAdd(qcount, 1u) : (unsigned)kQueue;
                     if (slot < (unsigned)kQueue) {
                         q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
                         q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
                         qcell[slot] = (unsigned)jrem;
                     } else {
                         deposit_remainder<T>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0], r2[1],
-                                             r2[2], kx, ky, kz, scale);
+                                             r2[2], kx, ky, kz, scale, fits);
                     }
                 }
 #endif
@@ -383,7 +398,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     const int nq = min(*qcount, (unsigned)kQueue);
     for (int e = tid; e < nq; e += NT) {
         deposit_remainder<T>(jt, (int)qcell[e], J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
-                             q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz, scale);
+                             q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz, scale, true);
     }
     const int nf = min(*fqcount, (unsigned)kFQueue);
     for (int e = tid; e < nf; e += NT) {
