@@ -50,7 +50,7 @@ def load_peaks():
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """Samples SM clock and throttle reasons with NVML every ~5 ms."""
+    """Samples SM clock and throttle reasons with NVML every ~1 ms."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -82,7 +82,7 @@ class ClockSampler:
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv:
