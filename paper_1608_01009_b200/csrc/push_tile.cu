@@ -419,17 +419,19 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     }
     __syncthreads();
     }   // species
-    // flush the fixed-point tile to the fp64 global J: one thread per (comp, z, y) row
+    // flush the fixed-point tile to the fp64 global J.  Lanes run along x (a
+    // warp covers 3 rows of TJ consecutive nodes, lanes 3 TJ.. idle): the tile
+    // reads hit consecutive banks and the REDGs of a row are coalesced
     const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
-    for (int row = tid; row < 3 * TJ * TJ; row += NT) {
-        const int comp = row / (TJ * TJ), c = (row / TJ) % TJ, b = row % TJ;
-        const int base = comp * NJ + c * JPY + b * JPX;
-        double *Jrow = J + comp * cs + gorigin + gsy * b + gsz * c;
-#pragma unroll
-        for (int a = 0; a < TJ; ++a) {
-            const long long fx = (long long)(int)jt[6 * NJ + base + a] * 4294967296LL +
-                                 (long long)jt[3 * NJ + base + a] * 65536LL + (long long)jt[base + a];
-            if (fx != 0) atomicAdd(Jrow + a, (double)fx * inv_scale);
+    constexpr int kRowsPerWarp = 32 / TJ;
+    const int wid = tid >> 5, a = lane % TJ, rsub = lane / TJ;
+    if (rsub < kRowsPerWarp) {
+        for (int row = wid * kRowsPerWarp + rsub; row < 3 * TJ * TJ; row += (NT / 32) * kRowsPerWarp) {
+            const int comp = row / (TJ * TJ), c = (row / TJ) % TJ, b = row % TJ;
+            const int node = comp * NJ + c * JPY + b * JPX + a;
+            const long long fx = (long long)(int)jt[6 * NJ + node] * 4294967296LL +
+                                 (long long)jt[3 * NJ + node] * 65536LL + (long long)jt[node];
+            if (fx != 0) atomicAdd(J + comp * cs + gorigin + gsy * b + gsz * c + a, (double)fx * inv_scale);
         }
     }
 }
