@@ -485,7 +485,10 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
     // supercells (> 8192 particles expected) are split over several CTAs --
     // splitting C2's 3200-particle supercells was measured slower (extra tile
     // loads and flushes outweigh the shorter last wave)
-    const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + 8191) / 8192));
+#ifndef PIC_SPLIT_AT
+#define PIC_SPLIT_AT 8192
+#endif
+    const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + PIC_SPLIT_AT - 1) / PIC_SPLIT_AT));
     const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)g.nsz);
     switch (ts.n) {
     case 1: k_push_tile<S, H, kGeneral, 1><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
