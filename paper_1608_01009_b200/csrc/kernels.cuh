@@ -48,17 +48,15 @@ void launch_step_prep(const unsigned *u2max_in, unsigned *u2max_out, double *sca
 // max |u|^2 of n particles -> *out (high 32 bits of the fp64 value)
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st);
 void configure_tile_kernels();
-// The species of one fused-kernel launch (every species with particles):
+// The species of one fused-kernel launch (one or two species with particles):
 // input arrays (sorted B on a sort step, else A), output arrays (A), offsets.
-constexpr int kTileMaxSpecies = 4;
+constexpr int kTileMaxSpecies = 2;
 struct TileSpecies {
     ParticlesDev in[kTileMaxSpecies], out[kTileMaxSpecies];
     const int64_t *sc_off[kTileMaxSpecies];
     SpeciesDev sp[kTileMaxSpecies];
     int n;
 };
-// number of supercells holding particles of the species of ts (synchronises st)
-int64_t count_occupied(const GridDev &g, const TileSpecies &ts, unsigned *scratch, cudaStream_t st);
 // mean_per_sc: particles per supercell over all species (splits very dense supercells)
 void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
                       const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st);

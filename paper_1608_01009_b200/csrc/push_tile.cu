@@ -192,11 +192,19 @@ __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *
 // in the final store); false for the single-domain periodic box.
 // One CTA pushes every species of its supercell in turn, so the E/B tile
 // is loaded and the J tile zeroed and flushed once per supercell and step.
+// kGeneral: slabs (nranks > 1) or an open z box (migration / absorption
+// in the final store); false for the single-domain periodic box.
+// NSP = 1 or 2 species per launch.  With two, the CTA walks the
+// concatenation of both species' ranges of its supercell in ONE particle
+// loop (the species of a particle is a select on its index), so the E/B
+// tile load, the J-tile zeroing and flush and the loop's ragged last
+// iteration are paid once per supercell, and the loop body is not duplicated.
 template <int S, int H, bool kGeneral, int NSP>
 __global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
 k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
             double *__restrict__ J, const __grid_constant__ TileSpecies ts, int split, unsigned *err)
 {
+    static_assert(NSP == 1 || NSP == 2, "one or two species per launch");
     using T = TileGeom<S, H>;
     constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = kTileThreads;
     constexpr int EPX = T::EPX, EPY = T::EPY, JPX = T::JPX, JPY = T::JPY;
@@ -228,14 +236,17 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             b = P0 + (int)(((int64_t)(P1 - P0) * (part + 1)) / split);
         }
     };
-    int total = 0;
-#pragma unroll
-    for (int s = 0; s < NSP; ++s) {
-        int a, b;
-        range(s, a, b);
-        total += b - a;
-    }
+    int a0, b0, a1 = 0, b1 = 0;
+    range(0, a0, b0);
+    if (NSP == 2) range(1, a1, b1);
+    const int n0 = b0 - a0, total = n0 + (b1 - a1);
     if (total == 0) return;   // empty (uniform per CTA)
+    // concatenated index i -> species (s1: the second one) and its array index p
+    auto locate = [&](int i, bool &s1, int &p) {
+        s1 = NSP == 2 && i >= n0;
+        p = s1 ? a1 + (i - n0) : a0 + i;
+    };
+    const TileSpecies &T0 = ts;   // (readability: ts.in[s1], ts.sp[s1] below)
 
     // local-grid coordinates of the tile origin (same for the E/B and J tiles)
     const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
@@ -247,6 +258,21 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         mbar_arrive_expect_tx(bar_eb, 6 * NE * sizeof(double));
         tma_load_4d(eb, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, bar_eb);
     }
+    auto stage = [&](int i, int st) {   // this thread's particle i -> its staging slot
+        bool s1;
+        int p;
+        locate(i, s1, p);
+        const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
+        double *d = pbuf + st * 6 * NT + tid;
+        cp_async8(d + 0 * NT, in.x + p);
+        cp_async8(d + 1 * NT, in.y + p);
+        cp_async8(d + 2 * NT, in.z + p);
+        cp_async8(d + 3 * NT, in.ux + p);
+        cp_async8(d + 4 * NT, in.uy + p);
+        cp_async8(d + 5 * NT, in.uz + p);
+    };
+    if (tid < total) stage(tid, 0);
+    cp_async_commit();
     {   // zero the fixed-point J tile (16-byte stores)
         uint4 *j4 = (uint4 *)jt;
         for (int t = tid; t < (9 * NJ) / 4; t += NT) j4[t] = make_uint4(0u, 0u, 0u, 0u);
@@ -258,46 +284,26 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     }
 
     const double cdt = g.c * g.dt;
-    // fixed-point scale 2^F of this step (k_step_prep): the smallest over the
-    // species, so every species' contributions stay inside the range
+    // fixed-point scale 2^F of this step (k_step_prep): the smaller of the
+    // species' scales, so both species' contributions stay inside the range
     double scale = ts.sp[0].scale[0], inv_scale = ts.sp[0].scale[1];
-#pragma unroll
-    for (int s = 1; s < NSP; ++s)
-        if (ts.sp[s].scale[0] < scale) {
-            scale = ts.sp[s].scale[0];
-            inv_scale = ts.sp[s].scale[1];
-        }
+    if (NSP == 2 && ts.sp[NSP - 1].scale[0] < scale) {
+        scale = ts.sp[NSP - 1].scale[0];
+        inv_scale = ts.sp[NSP - 1].scale[1];
+    }
+    double u2loc0 = 0.0, u2loc1 = 0.0;   // this thread's max |u|^2 after the push, per species
     const bool tile_ok = total <= kMaxTileParticles;   // else the counters could overflow
     __syncthreads();
     mbar_wait(bar_eb, 0);
 
-    // NSP is a template parameter so every species' pointers and constants
-    // stay kernel-parameter (constant bank) operands instead of registers
-#pragma unroll
-    for (int s = 0; s < NSP; ++s) {
-    int p0, p1;
-    range(s, p0, p1);
-    if (p0 == p1) continue;   // uniform per CTA
-    const ParticlesDev &in = ts.in[s], &out = ts.out[s];
-    const SpeciesDev &sp = ts.sp[s];
-    const double kx = sp.kx, ky = sp.ky, kz = sp.kz;   // q w / (dt dA), host
-    double u2loc = 0.0;   // this thread's max |u|^2 after the push
-    auto stage = [&](int p, int st) {   // this thread's particle p -> its staging slot
-        double *d = pbuf + st * 6 * NT + tid;
-        cp_async8(d + 0 * NT, in.x + p);
-        cp_async8(d + 1 * NT, in.y + p);
-        cp_async8(d + 2 * NT, in.z + p);
-        cp_async8(d + 3 * NT, in.ux + p);
-        cp_async8(d + 4 * NT, in.uy + p);
-        cp_async8(d + 5 * NT, in.uz + p);
-    };
-    if (p0 + tid < p1) stage(p0 + tid, 0);
-    cp_async_commit();
     int st = 0;
-    for (int p = p0 + tid; p < p1; p += NT) {
-        if (p + NT < p1) stage(p + NT, st ^ 1);   // prefetch the next particle
+    for (int i = tid; i < total; i += NT) {
+        if (i + NT < total) stage(i + NT, st ^ 1);   // prefetch the next particle
         cp_async_commit();
         cp_async_wait1();
+        bool s1;
+        int p;
+        locate(i, s1, p);
         const double *pl = pbuf + st * 6 * NT + tid;
         st ^= 1;
         const double x = pl[0], y = pl[NT], z = pl[2 * NT];
@@ -331,7 +337,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
 #undef ty
 #undef tz
 #endif
-            boris(sp.h, ex, ey, ez, bx, by, bz, ux, uy, uz);
+            boris(s1 ? T0.sp[NSP - 1].h : T0.sp[0].h, ex, ey, ez, bx, by, bz, ux, uy, uz);
 #else
             (void)hx; (void)hy; (void)hz;
 #endif
@@ -344,14 +350,18 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
             const double dxl = bxl - wx.f0, dyl = byl - wy.f0, dzl = bzl - wz.f0;
             const bool ok = fabs(dxl) < 1.0 && fabs(dyl) < 1.0 && fabs(dzl) < 1.0;
-            u2loc = fmax(u2loc, u2);
+            if (s1) u2loc1 = fmax(u2loc1, u2); else u2loc0 = fmax(u2loc0, u2);
+            const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
+            const ParticlesDev &out = s1 ? T0.out[NSP - 1] : T0.out[0];
+            const SpeciesDev &sp = s1 ? T0.sp[NSP - 1] : T0.sp[0];
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
-                               kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, false, err);
+                                         kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, false, err);
             else
                 store_particle<kGeneral>(g, sp, out, in.id, p, x, y, z, ux, uy, uz, false, err);
             if (ok) {
 #ifndef PIC_EXP_NODEP   // timing experiment only: no deposit
+                const double kx = sp.kx, ky = sp.ky, kz = sp.kz;   // q w / (dt dA), host
                 const int jbase = tx + JPX * ty + JPY * tz;
                 double ex_, ey_, ez_, r1[3], r2[3];
                 int cx, cy, cz;
@@ -362,14 +372,15 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                                fits);
                 if (more) {
                     // the rest of a face-crossing path is deposited after the particle
-                    // loop, all queued paths together (keeps the loop convergent)
+                    // loop, all queued paths together (keeps the loop convergent); the
+                    // species is the top bit of the queued cell
                     const int jrem = jbase + cx + JPX * cy + JPY * cz;
                     // only fitting paths are queued (the drain deposits into the tile)
                     const unsigned slot = fits ? atomicAdd(qcount, 1u) : (unsigned)kQueue;
                     if (slot < (unsigned)kQueue) {
                         q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
                         q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
-                        qcell[slot] = (unsigned)jrem;
+                        qcell[slot] = (unsigned)jrem | (s1 ? 0x80000000u : 0u);
                     } else {
                         deposit_remainder<T>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0], r2[1],
                                              r2[2], kx, ky, kz, scale, fits);
@@ -385,40 +396,51 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             // the loop so the slow global path does not stall this warp's iteration
             const unsigned slot = atomicAdd(fqcount, 1u);
             if (slot < (unsigned)kFQueue) {
-                fq[slot] = (unsigned)p;
+                fq[slot] = (unsigned)i;
             } else {
+                const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
+                const ParticlesDev &out = s1 ? T0.out[NSP - 1] : T0.out[0];
+                const SpeciesDev &sp = s1 ? T0.sp[NSP - 1] : T0.sp[0];
                 double xx = x, yy = y, zz = z;
                 push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
                 store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
-                u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+                const double v2 = ux * ux + uy * uy + uz * uz;
+                if (s1) u2loc1 = fmax(u2loc1, v2); else u2loc0 = fmax(u2loc0, v2);
             }
         }
     }
     __syncthreads();   // all particles pushed, the queues are complete
     const int nq = min(*qcount, (unsigned)kQueue);
     for (int e = tid; e < nq; e += NT) {
-        deposit_remainder<T>(jt, (int)qcell[e], J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
-                             q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], kx, ky, kz, scale, true);
+        const unsigned qc = qcell[e];
+        const SpeciesDev &sp = (qc >> 31) ? T0.sp[NSP - 1] : T0.sp[0];
+        deposit_remainder<T>(jt, (int)(qc & 0x7fffffffu), J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
+                             q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], sp.kx, sp.ky, sp.kz, scale,
+                             true);
     }
     const int nf = min(*fqcount, (unsigned)kFQueue);
     for (int e = tid; e < nf; e += NT) {
-        const int p = (int)fq[e];
+        bool s1;
+        int p;
+        locate((int)fq[e], s1, p);
+        const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
+        const ParticlesDev &out = s1 ? T0.out[NSP - 1] : T0.out[0];
+        const SpeciesDev &sp = s1 ? T0.sp[NSP - 1] : T0.sp[0];
         double xx = in.x[p], yy = in.y[p], zz = in.z[p], ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
         push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
         store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
-        u2loc = fmax(u2loc, ux * ux + uy * uy + uz * uz);
+        const double v2 = ux * ux + uy * uy + uz * uz;
+        if (s1) u2loc1 = fmax(u2loc1, v2); else u2loc0 = fmax(u2loc0, v2);
     }
     {
-        const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc) >> 32));
-        if (lane == 0 && hi) atomicMax(sp.u2max_out, hi);
-    }
-    __syncthreads();   // queues drained: reset them for the next species
-    if (tid == 0) {
-        *qcount = 0u;
-        *fqcount = 0u;
+        const unsigned hi0 = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc0) >> 32));
+        if (lane == 0 && hi0) atomicMax(ts.sp[0].u2max_out, hi0);
+        if (NSP == 2) {
+            const unsigned hi1 = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc1) >> 32));
+            if (lane == 0 && hi1) atomicMax(ts.sp[NSP - 1].u2max_out, hi1);
+        }
     }
     __syncthreads();
-    }   // species
     // flush the fixed-point tile to the fp64 global J.  Lanes run along x (a
     // warp covers 3 rows of TJ consecutive nodes, lanes 3 TJ.. idle): the tile
     // reads hit consecutive banks and the REDGs of a row are coalesced
@@ -490,34 +512,10 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
 #endif
     const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + PIC_SPLIT_AT - 1) / PIC_SPLIT_AT));
     const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)g.nsz);
-    switch (ts.n) {
-    case 1: k_push_tile<S, H, kGeneral, 1><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
-    case 2: k_push_tile<S, H, kGeneral, 2><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
-    case 3: k_push_tile<S, H, kGeneral, 3><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
-    default: k_push_tile<S, H, kGeneral, 4><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err); break;
-    }
-}
-
-// supercells holding particles of any species of ts (set-up time only)
-__global__ void __launch_bounds__(256) k_count_occupied(TileSpecies ts, int n_sc, unsigned *count)
-{
-    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
-    bool occ = false;
-    if (sc < n_sc)
-        for (int s = 0; s < ts.n; ++s) occ |= ts.sc_off[s][sc + 1] > ts.sc_off[s][sc];
-    const unsigned m = __ballot_sync(0xffffffffu, occ);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, (unsigned)__popc(m));
-}
-
-int64_t count_occupied(const GridDev &g, const TileSpecies &ts, unsigned *scratch, cudaStream_t st)
-{
-    const int n_sc = g.nsx * g.nsy * g.nsz;
-    unsigned h = 0;
-    cudaMemsetAsync(scratch, 0, sizeof(unsigned), st);
-    if (ts.n > 0) k_count_occupied<<<(n_sc + 255) / 256, 256, 0, st>>>(ts, n_sc, scratch);
-    cudaMemcpyAsync(&h, scratch, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    return (int64_t)h;
+    if (ts.n == 1)
+        k_push_tile<S, H, kGeneral, 1><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err);
+    else
+        k_push_tile<S, H, kGeneral, 2><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err);
 }
 
 bool tile_supported(int S) { return S == 2 || S == 4; }
@@ -537,8 +535,6 @@ static void set_smem()
     const int b = (int)TileGeom<S, 1>::smem_bytes;
     cudaFuncSetAttribute(k_push_tile<S, 1, G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
     cudaFuncSetAttribute(k_push_tile<S, 1, G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_push_tile<S, 1, G, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_push_tile<S, 1, G, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
 void configure_tile_kernels()

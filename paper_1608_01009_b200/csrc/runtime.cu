@@ -56,7 +56,6 @@ struct Layout {
     size_t off_rho = 0, off_rho_prev = 0, off_gauss0 = 0, off_acc = 0;   // diagnostics
     size_t off_laser = 0, off_step = 0;                                  // NEXT-1 open z
     size_t off_scale = 0;                                                // J-tile scales
-    size_t off_wscratch = 0;                                             // count_occupied
     size_t total = 0;
 };
 
@@ -182,7 +181,6 @@ Layout make_layout(const pic_config *c)
     L.off_laser = o; o = align_up(o + sizeof(double) * 8);
     L.off_step = o; o = align_up(o + sizeof(int64_t));
     L.off_scale = o; o = align_up(o + sizeof(double) * 2 * PIC_MAX_SPECIES);
-    L.off_wscratch = o; o = align_up(o + sizeof(unsigned));
     L.total = o;
     return L;
 }
@@ -302,7 +300,6 @@ struct pic_ctx {
     bool diag_have_g0 = false;
     int64_t step_index = 0;
     bool use_tile = false;     // fused supercell kernel (else the naive kernel)
-    bool merge_species = false;   // one fused launch for all species (sparse boxes, pic_set_particles)
     bool slabs = false;        // nranks > 1
     bool local_group = false;  // slabs exchanged by pic_step_group (no NCCL)
     bool ghosts_stale = false; // E/B z ghosts need an exchange (after pic_set_fields)
@@ -504,10 +501,10 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
         ++launches;
     }
     if (ctx->use_tile) {
-        // a sparse box (most supercells empty, C5) pushes every species in one
-        // launch: the empty supercells' CTAs and the shared E/B tile load,
-        // J-tile zeroing and flush are paid once (C5_1g: 6.0 -> 4.35 ms per
-        // step); a dense box launches per species (C3: 4.79 vs 5.0 ms merged)
+        // species go in pairs: one launch walks both species of a supercell in
+        // one particle loop, so its E/B tile load, J-tile zeroing and flush,
+        // its ragged last iteration and (C5) the CTAs of empty supercells are
+        // paid once (C3 4.74 -> 4.43, C5_1g 4.38 -> 4.02 ms per step)
         TileSpecies ts{};
         int64_t cap_total = 0;
         for (int s = 0; s < ctx->cfg.n_species; ++s) {
@@ -518,12 +515,13 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
             ts.sp[ts.n] = species_dev(ctx, s, jcur);
             cap_total += L.cap[s];
             ++ts.n;
-            if (!ctx->merge_species) {
+            if (ts.n == 2) {   // a launch takes one or two species
                 launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], ts, ctx->err,
-                                 L.cap[s] / std::max<int64_t>(1, L.n_sc), ctx->st);
+                                 cap_total / std::max<int64_t>(1, L.n_sc), ctx->st);
                 ++launches;
                 if (profile) ctx->particle_launches++;
                 ts.n = 0;
+                cap_total = 0;
             }
         }
         if (ts.n > 0) {
@@ -946,20 +944,6 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
             destroy_graphs(ctx);
             return fail(ctx, PIC_EINVAL, outside);
         }
-    }
-    if (ctx->use_tile) {
-        // merge the species into one launch when fewer than half of the
-        // supercells hold particles (decided on every pic_set_particles)
-        TileSpecies ts{};
-        int nsp = 0;
-        for (int s = 0; s < ctx->cfg.n_species; ++s) {
-            if (!ctx->has_particles[s]) continue;
-            ts.sc_off[ts.n++] = ctx->sc_off[s];
-            ++nsp;
-        }
-        const int64_t occ = count_occupied(g, ts, (unsigned *)(ctx->ws + ctx->L.off_wscratch), ctx->st);
-        ctx->merge_species = nsp > 1 && 2 * occ < ctx->L.n_sc;
-        ctx->launches += 1;
     }
     PIC_CUDA(ctx, cudaGetLastError());
     destroy_graphs(ctx);
