@@ -59,6 +59,7 @@ k_e_full(GridDev g, double *__restrict__ EB, double *__restrict__ Jc, double *__
     const int64_t o = pidx(g, i, j, k);
     // fold: the deposit of step n landed on the interior cell and its images
     double jx = 0.0, jy = 0.0, jz = 0.0;
+    int nimg = 0;
     for_images(g, i, j, k, [&](int64_t p) {
         jx += Jc[p];
         jy += Jc[cs + p];
@@ -66,10 +67,13 @@ k_e_full(GridDev g, double *__restrict__ EB, double *__restrict__ Jc, double *__
         Jn[p] = 0.0;
         Jn[cs + p] = 0.0;
         Jn[2 * cs + p] = 0.0;
+        ++nimg;
     });
-    Jc[o] = jx;
-    Jc[cs + o] = jy;
-    Jc[2 * cs + o] = jz;
+    if (nimg > 1) {   // the folded J (J^{n+1/2} for pic_get_fields); a cell without
+        Jc[o] = jx;   // images already holds it
+        Jc[cs + o] = jy;
+        Jc[2 * cs + o] = jz;
+    }
     const double bx = Bx[o], by = By[o], bz = Bz[o];
     const double cx = (bz - Bz[o - sy]) * g.inv_dy - (by - By[o - sz]) * g.inv_dz;
     const double cy = (bx - Bx[o - sz]) * g.inv_dz - (bz - Bz[o - 1]) * g.inv_dx;
