@@ -8,9 +8,11 @@
 //   1. loads the supercell's E/B tile plus a (1+H)-cell halo,
 //      (S+2H+2)^3 x 6 fp64, with ONE TMA tensor copy (mbarrier-tracked) from
 //      the ghost-padded fields into a bank-conflict-padded shared tile;
-//   2. streams its particles [sc_off[s], sc_off[s+1]) through per-thread
-//      cp.async (LDGSTS) staging, one particle ahead; the sort stores them
-//      slot-major, so the lanes of a warp sit in distinct cells;
+//   2. streams its particles -- the concatenation of the supercell's ranges
+//      [sc_off[s], sc_off[s+1]) of the one or two species of the launch --
+//      through per-thread cp.async (LDGSTS) staging, one particle ahead; the
+//      sort stores them slot-major, so the lanes of a warp sit in distinct
+//      cells;
 //   3. gathers E/B from the tile, does Boris + move (straight-line code),
 //      stores x, u with coalesced stores, and deposits the Villasenor-Buneman
 //      currents into a deterministic fixed-point J tile with native u32
@@ -246,7 +248,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         s1 = NSP == 2 && i >= n0;
         p = s1 ? a1 + (i - n0) : a0 + i;
     };
-    const TileSpecies &T0 = ts;   // (readability: ts.in[s1], ts.sp[s1] below)
 
     // local-grid coordinates of the tile origin (same for the E/B and J tiles)
     const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
@@ -262,7 +263,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         bool s1;
         int p;
         locate(i, s1, p);
-        const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
+        const ParticlesDev &in = s1 ? ts.in[NSP - 1] : ts.in[0];
         double *d = pbuf + st * 6 * NT + tid;
         cp_async8(d + 0 * NT, in.x + p);
         cp_async8(d + 1 * NT, in.y + p);
@@ -337,7 +338,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
 #undef ty
 #undef tz
 #endif
-            boris(s1 ? T0.sp[NSP - 1].h : T0.sp[0].h, ex, ey, ez, bx, by, bz, ux, uy, uz);
+            boris(s1 ? ts.sp[NSP - 1].h : ts.sp[0].h, ex, ey, ez, bx, by, bz, ux, uy, uz);
 #else
             (void)hx; (void)hy; (void)hz;
 #endif
@@ -351,9 +352,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double dxl = bxl - wx.f0, dyl = byl - wy.f0, dzl = bzl - wz.f0;
             const bool ok = fabs(dxl) < 1.0 && fabs(dyl) < 1.0 && fabs(dzl) < 1.0;
             if (s1) u2loc1 = fmax(u2loc1, u2); else u2loc0 = fmax(u2loc0, u2);
-            const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
-            const ParticlesDev &out = s1 ? T0.out[NSP - 1] : T0.out[0];
-            const SpeciesDev &sp = s1 ? T0.sp[NSP - 1] : T0.sp[0];
+            const ParticlesDev &in = s1 ? ts.in[NSP - 1] : ts.in[0];
+            const ParticlesDev &out = s1 ? ts.out[NSP - 1] : ts.out[0];
+            const SpeciesDev &sp = s1 ? ts.sp[NSP - 1] : ts.sp[0];
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
                                          kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, false, err);
@@ -398,9 +399,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             if (slot < (unsigned)kFQueue) {
                 fq[slot] = (unsigned)i;
             } else {
-                const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
-                const ParticlesDev &out = s1 ? T0.out[NSP - 1] : T0.out[0];
-                const SpeciesDev &sp = s1 ? T0.sp[NSP - 1] : T0.sp[0];
+                const ParticlesDev &in = s1 ? ts.in[NSP - 1] : ts.in[0];
+                const ParticlesDev &out = s1 ? ts.out[NSP - 1] : ts.out[0];
+                const SpeciesDev &sp = s1 ? ts.sp[NSP - 1] : ts.sp[0];
                 double xx = x, yy = y, zz = z;
                 push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
                 store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
@@ -413,7 +414,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     const int nq = min(*qcount, (unsigned)kQueue);
     for (int e = tid; e < nq; e += NT) {
         const unsigned qc = qcell[e];
-        const SpeciesDev &sp = (qc >> 31) ? T0.sp[NSP - 1] : T0.sp[0];
+        const SpeciesDev &sp = (qc >> 31) ? ts.sp[NSP - 1] : ts.sp[0];
         deposit_remainder<T>(jt, (int)(qc & 0x7fffffffu), J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
                              q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], sp.kx, sp.ky, sp.kz, scale,
                              true);
@@ -423,9 +424,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         bool s1;
         int p;
         locate((int)fq[e], s1, p);
-        const ParticlesDev &in = s1 ? T0.in[NSP - 1] : T0.in[0];
-        const ParticlesDev &out = s1 ? T0.out[NSP - 1] : T0.out[0];
-        const SpeciesDev &sp = s1 ? T0.sp[NSP - 1] : T0.sp[0];
+        const ParticlesDev &in = s1 ? ts.in[NSP - 1] : ts.in[0];
+        const ParticlesDev &out = s1 ? ts.out[NSP - 1] : ts.out[0];
+        const SpeciesDev &sp = s1 ? ts.sp[NSP - 1] : ts.sp[0];
         double xx = in.x[p], yy = in.y[p], zz = in.z[p], ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
         push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
         store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
