@@ -202,6 +202,21 @@ def test_tile_fallback_after_long_drift(pic, oracle_mod):
     _run_parity(pic, oracle_mod, wl, 30, teacher_forced=False, tol=1e-10)
 
 
+def test_two_species_launch_fallback_and_queues(pic, oracle_mod):
+    """Both species in one fused launch (one concatenated particle loop):
+    fast electrons and protons drift beyond the tile halo without re-sorts
+    (global fallback queue, species recovered from the queued index), cross
+    faces often (remainder queue, species in the queued cell's top bit), and
+    share the J tile with the smaller of the two fixed-point scales."""
+    from synth import get_config
+    from synth.configs import electron, proton
+    wl = get_config("C1").with_(species=(electron(3, 0.3), proton(2, 200.0)), sort_every=0,
+                                nx=16, ny=16, nz=8)
+    rng = np.random.default_rng(14)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.05
+    _run_parity(pic, oracle_mod, wl, 25, teacher_forced=False, fields=F6, tol=1e-10)
+
+
 def test_naive_flag_path(pic, oracle_mod):
     from synth import get_config
     wl = get_config("T_small")
