@@ -308,7 +308,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         const double *pl = pbuf + st * 6 * NT + tid;
         st ^= 1;
         const double x = pl[0], y = pl[NT], z = pl[2 * NT];
-        if (x < 0.0) continue;   // dead slot (migrated away since the last sort)
+        // dead slot (migrated away or absorbed since the last sort; a single
+        // periodic box has none)
+        if (kGeneral && x < 0.0) continue;
         double ux = pl[3 * NT], uy = pl[4 * NT], uz = pl[5 * NT];
         const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
         const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
