@@ -1,3 +1,7 @@
+#!/usr/bin/env python3
+"""Per-array diagnosis of the open-z laser case (T_laser) on the GPU: for the
+first steps, teacher-forced from the oracle, prints max |ref| and max |GPU -
+ref| of every field component and particle set (python tools/dbg_open.py)."""
 import sys, numpy as np
 sys.path.insert(0, '.')
 import paper_1608_01009_b200 as pic
