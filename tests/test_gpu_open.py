@@ -220,3 +220,52 @@ def test_open_unequal_slabs_match_single_domain_oracle(pic, oracle_mod, split):
             for r, P_r in enumerate(Ps):   # every particle lives in its rank's slab
                 assert (P_r[2] >= split[r]).all() and (P_r[2] < split[r + 1]).all()
         assert max(errs) <= 1e-10, (step, errs)
+
+
+def test_c5_1g_full_size_sampled_and_continuity(pic, oracle_mod):
+    """C5_1g (128 x 128 x 1024 open box, 104.9M particles, two species in one
+    launch) at full size in the bench launch configuration, 150 steps after
+    the preload (the a0 = 10 ramp is at 76% on the slab surface): sampled
+    particles of both species against the oracle's per-particle gather /
+    Boris / move on the GPU's own fields, at least some relativistic, and
+    discrete charge continuity of the deposit on the whole grid."""
+    from synth import gen_particles, get_config
+    O = oracle_mod
+    wl = get_config("C5_1g")
+    parts = gen_particles(wl)
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    del parts
+    sim.laser_preload()
+    sim.step(150)
+    F0 = sim.get_fields()
+    P0 = [sim.get_particles(s) for s in range(2)]
+    sim.step(1)
+    F1 = sim.get_fields()
+    P1 = [sim.get_particles(s) for s in range(2)]
+    orc = _oracle(O, wl, [(np.zeros((6, 0)), np.zeros(0, np.uint64))] * 2)
+    orc.F[:] = F0
+    L = np.array(_L(wl))
+    rng = np.random.default_rng(33)
+    umax = 0.0
+    for s, sp in enumerate(wl.species):
+        (A, ia), (B, ib) = P0[s], P1[s]
+        assert np.array_equal(ia, ib)            # no re-sort or absorption between the two states
+        for p in rng.choice(A.shape[1], 400, replace=False):
+            EB = orc.gather(*A[:3, p])
+            u = O.boris(sp.q, sp.m, wl.c, wl.dt, EB, A[3:, p])
+            xn = O.move(wl.c, wl.dt, u, A[:3, p])
+            xn[:2] = [O.wrap(xn[d], L[d]) for d in range(2)]
+            assert np.abs(B[3:, p] - u).max() <= TOL_STEP * max(np.abs(u).max(), 1e-300)
+            d = B[:3, p] - xn
+            d[:2] = (d[:2] + L[:2] / 2) % L[:2] - L[:2] / 2
+            assert np.abs(d).max() <= TOL_STEP * L.max()
+        umax = max(umax, float(np.abs(A[3:]).max()))
+    assert umax > 1.0, umax   # relativistic electrons in the slab
+    rho0 = sum(orc.rho_of(s, P0[s][0]) for s in range(2))
+    rho1 = sum(orc.rho_of(s, P1[s][0]) for s in range(2))
+    orc.F[6:] = F1[6:]
+    divj = orc.div_edge(6)
+    res = (rho1 - rho0) / wl.dt + divj
+    assert np.abs(res).max() <= 1e-12 * np.abs(divj).max() + 1e-15
