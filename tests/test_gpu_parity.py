@@ -488,3 +488,37 @@ def test_c3_full_size_two_species_sampled_and_continuity(pic, oracle_mod):
     divj = orc.div_edge(6)
     res = (rho1 - rho0) / wl.dt + divj
     assert np.abs(res).max() <= 1e-12 * np.abs(divj).max() + 1e-15
+
+
+def test_c4_full_size_sampled(pic, oracle_mod):
+    """C4 at N = 1 (256 x 256 x 128, 32 e per cell, 268M particles -- the
+    per-GPU shape of the weak-scaling bench) in the bench launch
+    configuration, 25 steps (one re-sort at step 20): sampled particles
+    against the oracle's per-particle gather / Boris / move on the GPU's own
+    fields."""
+    from synth import get_config, gen_particles
+    wl = get_config("C4")
+    parts = gen_particles(wl)
+    sim = _sim(pic, wl)
+    _load(sim, parts)
+    del parts
+    sim.step(25)
+    F0 = sim.get_fields()
+    A, ia = sim.get_particles(0)
+    sim.step(1)
+    B, ib = sim.get_particles(0)
+    assert np.array_equal(ia, ib)
+    orc = _oracle_for(oracle_mod, wl, [(np.zeros((6, 0)), np.zeros(0, np.uint64))])
+    orc.F[:] = F0
+    O = oracle_mod
+    L = np.array(_L(wl))
+    sp = wl.species[0]
+    rng = np.random.default_rng(35)
+    for p in rng.choice(A.shape[1], 800, replace=False):
+        EB = orc.gather(*A[:3, p])
+        u = O.boris(sp.q, sp.m, wl.c, wl.dt, EB, A[3:, p])
+        xn = O.move(wl.c, wl.dt, u, A[:3, p])
+        xn = np.array([O.wrap(xn[d], L[d]) for d in range(3)])
+        assert rel_err(B[3:, p], u) <= TOL_STEP
+        d = (B[:3, p] - xn + L / 2) % L - L / 2
+        assert np.abs(d).max() <= TOL_STEP * L.max()
