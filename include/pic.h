@@ -113,10 +113,11 @@ typedef struct pic_ctx pic_ctx;
 int pic_workspace_size(const pic_config *cfg, size_t *bytes);
 
 /* Validates cfg (dt <= 1/(c sqrt(1/dx^2+1/dy^2+1/dz^2)); S divides nx, ny and
- * nz/nranks; 1 <= n_species <= PIC_MAX_SPECIES; m > 0), carves d_workspace
+ * the slab thickness; 1 <= n_species <= PIC_MAX_SPECIES; m > 0), carves d_workspace
  * (device pointer, `bytes` long), sets up NCCL when nranks > 1 and zeroes
  * E, B, J and all particle counts.  The rank owns z in [rank*nz/nranks,
- * (rank+1)*nz/nranks).  *out receives the context. */
+ * (rank+1)*nz/nranks), or [slab_lo, slab_hi) when set.  *out receives the
+ * context. */
 int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **out);
 
 /* Copies n particles of `species` from HOST arrays (global physical
@@ -141,8 +142,9 @@ int pic_set_fields(pic_ctx *ctx, const double *f);
 int pic_step(pic_ctx *ctx, int64_t nsteps);
 
 /* nranks > 1: z-slab decomposition.  Rank r owns the
- * planes [r nz/nranks, (r+1) nz/nranks) (nz/nranks >= 4, divisible by S).
- * Each step exchanges with ranks r-1 and r+1 (periodic ring), over NCCL
+ * planes [r nz/nranks, (r+1) nz/nranks), or [slab_lo, slab_hi) (>= 4 planes,
+ * divisible by S).  Each step exchanges with ranks r-1 and r+1 (a periodic
+ * ring, cut between the last and the first rank for PIC_BC_OPEN), over NCCL
  * point-to-point on cfg->stream: the J ghost planes (added by the owner), the
  * particles whose z left the slab (fixed-capacity buffers, migrate_capacity
  * per species and direction; overflow -> PIC_ECAPACITY), and the E and B
