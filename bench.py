@@ -273,11 +273,9 @@ def run_ours(args, wl, rank, world, local):
     from synth import gen_particles
 
     torch.cuda.set_device(local)
-    nccl_id = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        nccl_id = pkg.broadcast_nccl_id(pkg.nccl_unique_id() if rank == 0 else bytes(128))
     split = slab_split(wl, world)
     slab = (split[rank], split[rank + 1])
     if world > 1:
@@ -287,6 +285,11 @@ def run_ours(args, wl, rank, world, local):
     n_local = sum(p.shape[1] for p, _ in parts)
 
     def new_sim(flags=0):
+        # every context gets its own NCCL communicator, so a fresh unique id
+        # (an id bootstraps exactly one ncclCommInitRank); collective over ranks
+        nccl_id = None
+        if world > 1:
+            nccl_id = pkg.broadcast_nccl_id(pkg.nccl_unique_id() if rank == 0 else bytes(128))
         return pkg.simulation_from_workload(wl, capacity_factor=1.0, flags=flags, rank=rank,
                                             nranks=world, nccl_id=nccl_id, slab=slab)
 
