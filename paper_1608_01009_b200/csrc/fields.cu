@@ -16,7 +16,17 @@
 
 namespace pic {
 
-__global__ void __launch_bounds__(256) k_b_half(GridDev g, double *__restrict__ EB, double coef, int kbegin)
+// B half step(s) with the curl of E (the E of EB):
+//   B1 = Bin - coef curl E   -> Bout1
+//   B2 = B1  - coef curl E   -> Bout2 (when Bout2 != nullptr)
+// The step's second half (B^{n+1}, read by the particle kernel) and the next
+// step's first half (B^{n+3/2}, read by the next E update) use the same
+// curl E^{n+1}, so one pass writes both: the same two fma's, in the same
+// order, as two separate half steps.  Bin may alias Bout2 (each thread reads
+// only its own cell of Bin).
+__global__ void __launch_bounds__(256)
+k_b_half(GridDev g, const double *__restrict__ EB, const double *Bin, double *Bout1, double *Bout2,
+         double coef, int kbegin)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
@@ -24,30 +34,38 @@ __global__ void __launch_bounds__(256) k_b_half(GridDev g, double *__restrict__ 
     if (i >= g.nx || j >= g.ny) return;
     const int64_t cs = g.cs, sy = g.X, sz = (int64_t)g.X * g.Y;
     const double *Ex = EB, *Ey = EB + cs, *Ez = EB + 2 * cs;
-    double *Bx = EB + 3 * cs, *By = EB + 4 * cs, *Bz = EB + 5 * cs;
     const int64_t o = pidx(g, i, j, k);
     const double ex = Ex[o], ey = Ey[o], ez = Ez[o];
     const double cx = (Ez[o + sy] - ez) * g.inv_dy - (Ey[o + sz] - ey) * g.inv_dz;
     const double cy = (Ex[o + sz] - ex) * g.inv_dz - (Ez[o + 1] - ez) * g.inv_dx;
     const double cz = (Ey[o + 1] - ey) * g.inv_dx - (Ex[o + sy] - ex) * g.inv_dy;
-    const double bx = fma(-coef, cx, Bx[o]);
-    const double by = fma(-coef, cy, By[o]);
-    const double bz = fma(-coef, cz, Bz[o]);
     // open z (NEXT-1): Bx, By of the top plane sit at z = zmax + dz/2, outside
     // the box; they are not advanced
     const bool outside = g.open_hi && k == g.nz - 1;
+    const double bx0 = Bin[o], by0 = Bin[cs + o], bz0 = Bin[2 * cs + o];
+    const double bx = outside ? bx0 : fma(-coef, cx, bx0);
+    const double by = outside ? by0 : fma(-coef, cy, by0);
+    const double bz = fma(-coef, cz, bz0);
     for_images(g, i, j, k, [&](int64_t p) {
-        if (!outside) {
-            Bx[p] = bx;
-            By[p] = by;
-        }
-        Bz[p] = bz;
+        Bout1[p] = bx;
+        Bout1[cs + p] = by;
+        Bout1[2 * cs + p] = bz;
     });
+    if (Bout2) {
+        const double bx2 = outside ? bx : fma(-coef, cx, bx);
+        const double by2 = outside ? by : fma(-coef, cy, by);
+        const double bz2 = fma(-coef, cz, bz);
+        for_images(g, i, j, k, [&](int64_t p) {
+            Bout2[p] = bx2;
+            Bout2[cs + p] = by2;
+            Bout2[2 * cs + p] = bz2;
+        });
+    }
 }
 
 __global__ void __launch_bounds__(256)
-k_e_full(GridDev g, double *__restrict__ EB, double *__restrict__ Jc, double *__restrict__ Jn,
-         double coefE, double coefJ)
+k_e_full(GridDev g, double *__restrict__ EB, const double *__restrict__ Bh, double *__restrict__ Jc,
+         double *__restrict__ Jn, double coefE, double coefJ)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
@@ -55,7 +73,7 @@ k_e_full(GridDev g, double *__restrict__ EB, double *__restrict__ Jc, double *__
     if (i >= g.nx || j >= g.ny) return;
     const int64_t cs = g.cs, sy = g.X, sz = (int64_t)g.X * g.Y;
     double *Ex = EB, *Ey = EB + cs, *Ez = EB + 2 * cs;
-    const double *Bx = EB + 3 * cs, *By = EB + 4 * cs, *Bz = EB + 5 * cs;
+    const double *Bx = Bh, *By = Bh + cs, *Bz = Bh + 2 * cs;   // B^{n+1/2}
     const int64_t o = pidx(g, i, j, k);
     // fold: the deposit of step n landed on the interior cell and its images
     double jx = 0.0, jy = 0.0, jz = 0.0;
@@ -214,18 +232,19 @@ static dim3 field_grid(const GridDev &g, dim3 bs)
     return dim3((g.nx + bs.x - 1) / bs.x, (g.ny + bs.y - 1) / bs.y, g.nz);
 }
 
-void launch_b_half(const GridDev &g, double *EB, cudaStream_t st, int kbegin)
+void launch_b_half(const GridDev &g, const double *EB, const double *Bin, double *Bout1, double *Bout2,
+                   cudaStream_t st, int kbegin)
 {
     const dim3 bs(32, 8, 1);
     dim3 grid = field_grid(g, bs);
     grid.z = g.nz - kbegin;
-    k_b_half<<<grid, bs, 0, st>>>(g, EB, 0.5 * g.c * g.dt, kbegin);
+    k_b_half<<<grid, bs, 0, st>>>(g, EB, Bin, Bout1, Bout2, 0.5 * g.c * g.dt, kbegin);
 }
 
-void launch_e_full(const GridDev &g, double *EB, double *Jcur, double *Jnext, cudaStream_t st)
+void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext, cudaStream_t st)
 {
     const dim3 bs(32, 8, 1);
-    k_e_full<<<field_grid(g, bs), bs, 0, st>>>(g, EB, Jcur, Jnext, g.c * g.dt,
+    k_e_full<<<field_grid(g, bs), bs, 0, st>>>(g, EB, Bh, Jcur, Jnext, g.c * g.dt,
                                                 4.0 * M_PI * g.dt);
 }
 

@@ -8,13 +8,15 @@
 namespace pic {
 
 // ---- fields.cu : Yee FDTD and ghost maintenance ----
-// B -= (c dt/2) curl E on planes [kbegin, nz) (kbegin = -1 computes the lower
-// z ghost plane of a slab locally), result also stored to its ghost images.
-void launch_b_half(const GridDev &g, double *EB, cudaStream_t st, int kbegin = 0);
-// E += c dt curl B - 4 pi dt J where J = sum of the ghost images of Jcur
-// (the fold); writes the folded J back into Jcur's interior,
-// stores E to its ghost images and zeroes every image of Jnext.
-void launch_e_full(const GridDev &g, double *EB, double *Jcur, double *Jnext, cudaStream_t st);
+// Bout1 = Bin - (c dt/2) curl E (E of EB), and with Bout2 also Bout2 = Bout1 -
+// (c dt/2) curl E, on planes [kbegin, nz) (kbegin = -1 computes the lower z
+// ghost plane of a slab locally); results also stored to their ghost images.
+void launch_b_half(const GridDev &g, const double *EB, const double *Bin, double *Bout1, double *Bout2,
+                   cudaStream_t st, int kbegin = 0);
+// E += c dt curl Bh - 4 pi dt J (Bh = B^{n+1/2}) where J = sum of the ghost
+// images of Jcur (the fold); writes the folded J back into
+// Jcur's interior, stores E to its ghost images and zeroes every image of Jnext.
+void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext, cudaStream_t st);
 // Copies interior values of `ncomp` components to their ghost images.
 void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st);
 // NEXT-1 (open z): laser = {e0, omega, ramp, t0, pol_x, pol_y}.  Writes the

@@ -48,7 +48,7 @@ struct Layout {
     int64_t cap[PIC_MAX_SPECIES] = {};
     int64_t cap_max = 0;
     int64_t mig = 0;   // migration capacity (per species and direction), 0 on one rank
-    size_t off_eb = 0, off_j[2] = {}, off_sp[PIC_MAX_SPECIES][2] = {}, off_scoff[PIC_MAX_SPECIES] = {};
+    size_t off_eb = 0, off_bh = 0, off_j[2] = {}, off_sp[PIC_MAX_SPECIES][2] = {}, off_scoff[PIC_MAX_SPECIES] = {};
     size_t off_key = 0, off_slot = 0, off_perm_tmp = 0, off_perm = 0, off_count = 0, off_start = 0,
            off_bsums = 0, off_bsums2 = 0, off_err = 0, off_stat = 0, off_n = 0;
     size_t off_msend[PIC_MAX_SPECIES][2] = {}, off_mrecv[PIC_MAX_SPECIES][2] = {}, off_mcnt = 0;
@@ -140,6 +140,7 @@ Layout make_layout(const pic_config *c)
     size_t o = 0;
     L.off_eb = o; o = align_up(o + sizeof(double) * 6 * (size_t)g.cs);
     for (int b = 0; b < 2; ++b) { L.off_j[b] = o; o = align_up(o + sizeof(double) * 3 * (size_t)g.cs); }
+    L.off_bh = o; o = align_up(o + sizeof(double) * 3 * (size_t)g.cs);   // B^{n+1/2}
     for (int s = 0; s < c->n_species; ++s) {
         L.cap[s] = c->capacity[s];
         L.cap_max = std::max(L.cap_max, L.cap[s]);
@@ -276,6 +277,8 @@ struct pic_ctx {
     char *ws = nullptr;
     cudaStream_t st = nullptr;
     double *EB = nullptr;
+    double *Bh = nullptr;      // B^{n+1/2} for the next E update (bit-equal to a half step of EB's B)
+    bool bh_stale = false;     // Bh must be recomputed from EB (after pic_set_fields / pic_laser_preload)
     double *J[2] = {nullptr, nullptr};
     int jcur = 0;              // J buffer receiving the next deposit
     int jlast = 1;             // J buffer holding J^{n-1/2}
@@ -570,22 +573,36 @@ int phase_fields_e(pic_ctx *ctx, int jcur, bool profile)
             launches += 2;
         }
     }
-    // slabs compute the lower ghost plane of B^{n+1/2} locally, except below an
-    // open face (it lies outside the box and stays 0)
-    launch_b_half(g, ctx->EB, ctx->st, ctx->slabs && !g.open_lo ? -1 : 0);
+    // B^{n+1/2} is already in Bh (written by the previous step's phase_fields_b)
     if (g.open_lo) {
         launch_laser_coeffs(g, ctx->laser_par, ctx->dev_step, ctx->laser, ctx->st);
         ++launches;
     }
-    launch_e_full(g, ctx->EB, ctx->J[jcur], ctx->J[1 - jcur], ctx->st);
-    return launches + 2;
+    launch_e_full(g, ctx->EB, ctx->Bh, ctx->J[jcur], ctx->J[1 - jcur], ctx->st);
+    return launches + 1;
 }
 
+// slabs compute the lower ghost plane of Bh locally, except below an open face
+// (it lies outside the box and stays 0)
+int bh_kbegin(const pic_ctx *ctx) { return ctx->slabs && !ctx->L.g.open_lo ? -1 : 0; }
+
+// the second half step of this step and the first half step of the next one
+// in one pass: B^{n+1} -> EB, B^{n+3/2} -> Bh
 int phase_fields_b(pic_ctx *ctx, bool profile)
 {
     StageMark m(ctx, 2, profile);
-    launch_b_half(ctx->L.g, ctx->EB, ctx->st, 0);
+    launch_b_half(ctx->L.g, ctx->EB, ctx->Bh, ctx->EB + 3 * ctx->L.g.cs, ctx->Bh, ctx->st, bh_kbegin(ctx));
     return 1;
+}
+
+// Bh = B^n - (c dt/2) curl E^n from EB (once after EB was set from the host);
+// needs valid E ghosts
+void refresh_bh(pic_ctx *ctx)
+{
+    if (!ctx->bh_stale) return;
+    launch_b_half(ctx->L.g, ctx->EB, ctx->EB + 3 * ctx->L.g.cs, ctx->Bh, nullptr, ctx->st, bh_kbegin(ctx));
+    ctx->launches += 1;
+    ctx->bh_stale = false;
 }
 
 // a whole step on one rank (NCCL exchanges or none); returns launches or < 0
@@ -799,6 +816,7 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->slabs = cfg->nranks > 1;
     ctx->local_group = ctx->slabs && (cfg->flags & PIC_FLAG_LOCAL_GROUP);
     ctx->EB = (double *)(ctx->ws + L.off_eb);
+    ctx->Bh = (double *)(ctx->ws + L.off_bh);
     ctx->J[0] = (double *)(ctx->ws + L.off_j[0]);
     ctx->J[1] = (double *)(ctx->ws + L.off_j[1]);
     ctx->u2max[0] = (unsigned *)(ctx->ws + L.off_stat);
@@ -967,6 +985,7 @@ int pic_set_fields(pic_ctx *ctx, const double *f)
     launch_fill_ghosts(g, ctx->EB, 6, ctx->st);
     ctx->launches += 1;
     ctx->ghosts_stale = ctx->slabs;   // z ghost planes come from the neighbours
+    ctx->bh_stale = true;
     PIC_CUDA(ctx, cudaGetLastError());
     PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return PIC_OK;
@@ -1072,6 +1091,7 @@ int pic_step(pic_ctx *ctx, int64_t nsteps)
         if (rc != PIC_OK) return rc;
         ctx->ghosts_stale = false;
     }
+    if (nsteps > 0) refresh_bh(ctx);
     for (int64_t s = 0; s < nsteps; ++s) {
         const bool sort_now = K > 0 && (ctx->step_index % K) == 0;
         const int jc = ctx->jcur;
@@ -1118,6 +1138,8 @@ int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps)
         if (rc != PIC_OK) return rc;
         for (int r = 0; r < n; ++r) ctxs[r]->ghosts_stale = false;
     }
+    if (nsteps > 0)
+        for (int r = 0; r < n; ++r) refresh_bh(ctxs[r]);
     for (int64_t s = 0; s < nsteps; ++s) {
         const int64_t K = ctxs[0]->cfg.sort_every;
         const bool sort_now = K > 0 && (ctxs[0]->step_index % K) == 0;
@@ -1203,6 +1225,7 @@ int pic_laser_preload(pic_ctx *ctx)
     launch_laser_preload(ctx->L.g, ctx->laser_par, ctx->EB, ctx->st);
     ctx->launches += 1;
     ctx->ghosts_stale = ctx->slabs;   // z ghost planes come from the neighbours
+    ctx->bh_stale = true;
     PIC_CUDA(ctx, cudaGetLastError());
     PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return PIC_OK;
