@@ -446,17 +446,25 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     __syncthreads();
     // flush the fixed-point tile to the fp64 global J.  Lanes run along x (a
     // warp covers 3 rows of TJ consecutive nodes, lanes 3 TJ.. idle): the tile
-    // reads hit consecutive banks and the REDGs of a row are coalesced
+    // reads hit consecutive banks and the REDGs of a row are coalesced.
     const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
     constexpr int kRowsPerWarp = 32 / TJ;
     const int wid = tid >> 5, a = lane % TJ, rsub = lane / TJ;
+    // a warp takes whole (component, z) planes of the tile, kRowsPerWarp rows
+    // at a time, with the plane's base addresses computed once
     if (rsub < kRowsPerWarp) {
-        for (int row = wid * kRowsPerWarp + rsub; row < 3 * TJ * TJ; row += (NT / 32) * kRowsPerWarp) {
-            const int comp = row / (TJ * TJ), c = (row / TJ) % TJ, b = row % TJ;
-            const int node = comp * NJ + c * JPY + b * JPX + a;
-            const long long fx = (long long)(int)jt[6 * NJ + node] * 4294967296LL +
-                                 (long long)jt[3 * NJ + node] * 65536LL + (long long)jt[node];
-            if (fx != 0) atomicAdd(J + comp * cs + gorigin + gsy * b + gsz * c + a, (double)fx * inv_scale);
+        for (int pl = wid; pl < 3 * TJ; pl += NT / 32) {
+            const int comp = (pl >= TJ) + (pl >= 2 * TJ), c = pl - comp * TJ;
+            const unsigned *jn = jt + comp * NJ + c * JPY + a + rsub * JPX;
+            double *gp = J + comp * cs + gorigin + gsz * c + a + gsy * rsub;
+#pragma unroll
+            for (int r = 0; r < (TJ + kRowsPerWarp - 1) / kRowsPerWarp; ++r) {
+                if (TJ % kRowsPerWarp != 0 && rsub + r * kRowsPerWarp >= TJ) break;
+                const int o = r * kRowsPerWarp * JPX;
+                const long long fx = (long long)(int)jn[6 * NJ + o] * 4294967296LL +
+                                     (long long)jn[3 * NJ + o] * 65536LL + (long long)jn[o];
+                if (fx != 0) atomicAdd(gp + gsy * (r * kRowsPerWarp), (double)fx * inv_scale);
+            }
         }
     }
 }
