@@ -15,6 +15,7 @@
 //      position sum_c' min(n_c', r) + #{c' < c : n_c' > r}, so a warp of
 //      consecutive particles holds distinct cells (conflict-free shared
 //      atomics in the deposit)
+//   (4 and 5 run as one kernel per supercell in shared memory, k_order_sc)
 //   6. gather x,y,z,ux,uy,uz,id through the final permutation;
 //      sc_off[s] = start[s * S^3].
 // The key uses floor(x / dx) with an IEEE division, the same decision the
@@ -350,6 +351,134 @@ k_interleave(const uint32_t *__restrict__ start, int cps, const uint32_t *__rest
     }
 }
 
+// Steps 4 + 5 in one kernel, one CTA per supercell: the supercell's entries
+// of perm_tmp are staged in shared memory (a global scratch range for a
+// supercell holding more than kOrderCap), each cell's bucket is put in
+// ascending order by one warp, and the slot-major order is written back to
+// perm_tmp one slot layer per warp (coalesced).  Same result as
+// k_bucket_order + k_interleave.
+constexpr int kOrderThreads = 256;
+constexpr int kOrderCap = 4096;     // entries staged in shared memory
+constexpr int kOrderSlots = 256;    // slot layers with tables (cps <= 64)
+
+// a warp puts m = e - s entries of src[s..e) in ascending order into dst[s..)
+__device__ __forceinline__ void warp_order_bucket(const uint32_t *src, uint32_t *dst, uint32_t s, uint32_t m)
+{
+    const int lane = threadIdx.x & 31;
+    if (m == 1) {
+        if (lane == 0) dst[s] = src[s];
+    } else if (m <= 32) {
+        uint32_t k = (uint32_t)lane < m ? src[s + lane] : 0xffffffffu;
+        // often already in order (the counter atomics arrive roughly in index order)
+        const uint32_t nx = __shfl_down_sync(0xffffffffu, k, 1);
+        if (!__all_sync(0xffffffffu, lane == 31 || k <= nx)) k = warp_sort32(k);
+        if ((uint32_t)lane < m) dst[s + lane] = k;
+    } else if (m <= 64) {
+        uint32_t k0 = (uint32_t)lane < m ? src[s + lane] : 0xffffffffu;
+        uint32_t k1 = (uint32_t)lane + 32 < m ? src[s + 32 + lane] : 0xffffffffu;
+        const uint32_t n0 = __shfl_down_sync(0xffffffffu, k0, 1), n1 = __shfl_down_sync(0xffffffffu, k1, 1);
+        const uint32_t f1 = __shfl_sync(0xffffffffu, k1, 0);
+        if (!__all_sync(0xffffffffu, (lane == 31 ? k0 <= f1 : k0 <= n0) && (lane == 31 || k1 <= n1)))
+            warp_sort64(k0, k1);
+        if ((uint32_t)lane < m) dst[s + lane] = k0;
+        if ((uint32_t)lane + 32 < m) dst[s + 32 + lane] = k1;
+    } else {
+        for (uint32_t i0 = 0; i0 < m; i0 += 32) {
+            const bool mine = i0 + lane < m;
+            const uint32_t v = mine ? src[s + i0 + lane] : 0u;
+            uint32_t rank = 0;
+            for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+                const uint32_t u = (j0 + lane < m) ? src[s + j0 + lane] : 0xffffffffu;
+                const uint32_t cnt = min(32u, m - j0);
+                for (uint32_t t = 0; t < cnt; ++t) rank += (__shfl_sync(0xffffffffu, u, (int)t) < v) ? 1u : 0u;
+            }
+            if (mine) dst[s + rank] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kOrderThreads)
+k_order_sc(const uint32_t *__restrict__ start, int cps, uint32_t *perm_tmp, uint32_t *scratch)
+{
+    extern __shared__ uint32_t sh[];
+    uint32_t *cnt = sh;                        // [cps]
+    uint32_t *cum = cnt + cps;                 // [cps + 1]
+    uint32_t *buf = cum + cps + 1;             // [kOrderCap] staged input
+    uint32_t *srt = buf + kOrderCap;           // [kOrderCap] bucket-ordered
+    __shared__ unsigned long long mask[kOrderSlots];
+    __shared__ uint32_t sbase[kOrderSlots + 1];
+    __shared__ uint32_t maxcnt;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int kWarps = kOrderThreads / 32;
+    const int64_t c0 = (int64_t)blockIdx.x * cps;
+    const uint32_t base = start[c0];
+    const uint32_t n = start[c0 + cps] - base;
+    if (n == 0) return;   // uniform per CTA
+    if (tid == 0) maxcnt = 0;
+    for (int c = tid; c <= cps; c += kOrderThreads) {
+        cum[c] = start[c0 + c] - base;
+        if (c < cps) cnt[c] = start[c0 + c + 1] - start[c0 + c];
+    }
+    const bool staged = n <= (uint32_t)kOrderCap;
+    const uint32_t *src = staged ? buf : perm_tmp + base;
+    uint32_t *dst = staged ? srt : scratch + base;
+    if (staged)
+        for (uint32_t i = tid; i < n; i += kOrderThreads) buf[i] = perm_tmp[base + i];
+    __syncthreads();
+    for (int c = tid; c < cps; c += kOrderThreads) atomicMax(&maxcnt, cnt[c]);
+    for (int c = wid; c < cps; c += kWarps) {
+        const uint32_t m = cnt[c];
+        if (m) warp_order_bucket(src, dst, cum[c], m);
+    }
+    __syncthreads();
+    const uint32_t R = maxcnt;
+    if (cps <= 64 && R <= (uint32_t)kOrderSlots) {
+        // mask[r] = cells holding more than r particles, sbase[r] = particles in
+        // slots < r; layer r is written at sbase[r].. in ascending cell order
+        for (uint32_t r = wid; r < R; r += kWarps) {
+            const unsigned lo = __ballot_sync(0xffffffffu, lane < cps && cnt[lane] > r);
+            const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < cps && cnt[lane + 32] > r);
+            if (lane == 0) mask[r] = ((unsigned long long)hi << 32) | lo;
+        }
+        __syncthreads();
+        if (wid == 0) {   // exclusive scan of popc(mask[r])
+            uint32_t carry = 0;
+            for (uint32_t r0 = 0; r0 < R; r0 += 32) {
+                const uint32_t r = r0 + lane;
+                const uint32_t v = r < R ? (uint32_t)__popcll(mask[r]) : 0u;
+                const uint32_t inc = warp_incl_scan(v);
+                if (r < R) sbase[r] = carry + inc - v;
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        __syncthreads();
+        for (uint32_t r = wid; r < R; r += kWarps) {
+            const unsigned long long m = mask[r];
+            const uint32_t sb = base + sbase[r];
+            for (int c = lane; c < cps; c += 32)
+                if ((m >> c) & 1ull) perm_tmp[sb + __popcll(m & ((1ull << c) - 1ull))] = dst[cum[c] + r];
+        }
+    } else {
+        // wide supercells (S^3 > 64) or very full cells: the position of
+        // (cell c, slot r) is sum_c' min(n_c', r) + #{c' < c : n_c' > r}
+        for (uint32_t q = tid; q < n; q += kOrderThreads) {
+            int lo = 0, hi = cps;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (cum[mid] <= q) lo = mid; else hi = mid;
+            }
+            const int c = lo;
+            const uint32_t r = q - cum[c];
+            uint32_t pos = 0;
+            for (int cc = 0; cc < cps; ++cc) {
+                const uint32_t m = cnt[cc];
+                pos += min(m, r) + ((cc < c && m > r) ? 1u : 0u);
+            }
+            perm_tmp[base + pos] = dst[q];
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256)
 k_gather(ParticlesDev src, ParticlesDev dst, const uint32_t *__restrict__ perm,
          const uint32_t *__restrict__ live)
@@ -453,14 +582,20 @@ void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDe
     k_scan_blocks<<<1, kScanThreads, 0, st>>>(s.block_sums, nb);
     k_scan_add<<<(unsigned)nb, kScanThreads, 0, st>>>(s.count, nscan, s.block_sums, s.start);
     k_scatter<<<pblocks, bs, 0, st>>>(s.key, s.slot, s.start, dev_n, s.perm_tmp);
-    const int64_t threads = ncells * 32;
-    k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);
     const int cps = g.S * g.S * g.S;
-    k_interleave<<<(unsigned)n_sc, bs, sizeof(uint32_t) * (2 * cps + 1), st>>>(s.start, cps, s.perm,
-                                                                           s.perm_tmp);
+    const size_t order_smem = sizeof(uint32_t) * (2 * (size_t)cps + 1 + 2 * kOrderCap);
+    if (order_smem <= 48 * 1024) {
+        k_order_sc<<<(unsigned)n_sc, kOrderThreads, order_smem, st>>>(s.start, cps, s.perm_tmp, s.perm);
+    } else {   // very wide supercells: two passes through global memory
+        const int64_t threads = ncells * 32;
+        k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);
+        k_interleave<<<(unsigned)n_sc, bs, sizeof(uint32_t) * (2 * cps + 1), st>>>(s.start, cps, s.perm,
+                                                                               s.perm_tmp);
+        L += 1;
+    }
     k_gather<<<pblocks, bs, 0, st>>>(src, dst, s.perm_tmp, s.start + ncells);
     k_sc_offsets<<<(unsigned)((n_sc + 1 + bs - 1) / bs), bs, 0, st>>>(s.start, n_sc, cps, sc_off, dev_n);
-    L += 10;
+    L += 9;
     if (launches) *launches += L;
 }
 
