@@ -47,6 +47,20 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# fp64 work of one particle update: 336 flop (FMA = 2), the paper's VTune
+# count (PAPER.md:190 with Table 6 times)
+FLOP_PER_UPDATE = 336.0
+
+
+def load_fp64_peak():
+    """DFMA peak measured on a B200 by tools/microbench.cu (TFLOP/s)."""
+    p = os.path.join(ROOT, "profiles", "r01", "microbench.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["dfma_tflops"]), "measured (profiles/r01/microbench.json dfma_tflops)"
+    return 37.2, "datasheet (148 SM x 64 FP64 lanes x 2 x 1.965 GHz), not measured"
+
+
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
@@ -347,6 +361,8 @@ def run_ours(args, wl, rank, world, local):
     per_launch_ms = st["particle"] / n_launch
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     peak, peak_src = load_peaks()
+    fp64_peak, fp64_src = load_fp64_peak()
+    n_cells_local = wl.nx * wl.ny * (slab[1] - slab[0])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_particle_traffic.json")
     if os.path.exists(tp):   # ncu dram read + write of one launch, per workload
@@ -411,8 +427,15 @@ def run_ours(args, wl, rank, world, local):
                          "step_share": st["particle"] / max(1e-9, step_ms_prof * args.steps),
                          "stage_ms_per_step": {k: st[k] / args.steps for k in
                                                ("sort", "particle", "field", "exchange")},
-                         "whole_step_frac": (alg_bytes_total + n_local * 112.0 / max(wl.sort_every, 1))
-                         / (t_ms * 1e-3 / args.steps) / 1e9 / peak},
+                         # whole step: particle kernel bytes + sort (112 B/particle per
+                         # sort) + the Yee update (read E, B, J, write E, B: 120 B/cell)
+                         "whole_step_frac": (alg_bytes_total + n_local * 112.0 / max(wl.sort_every, 1)
+                                             + n_cells_local * 120.0)
+                         / (t_ms * 1e-3 / args.steps) / 1e9 / peak,
+                         # the second roof (report both fractions)
+                         "fp64": {"achieved_tflops": value / world * FLOP_PER_UPDATE / 1e12,
+                                  "peak_tflops": fp64_peak, "frac": value / world * FLOP_PER_UPDATE / 1e12 / fp64_peak,
+                                  "flop_per_update": FLOP_PER_UPDATE, "peak_source": fp64_src}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
