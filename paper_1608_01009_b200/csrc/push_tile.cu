@@ -379,7 +379,18 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                     // species is the top bit of the queued cell
                     const int jrem = jbase + cx + JPX * cy + JPY * cz;
                     // only fitting paths are queued (the drain deposits into the tile)
-                    const unsigned slot = fits ? atomicAdd(qcount, 1u) : (unsigned)kQueue;
+                    // one shared atomic per warp for the lanes that queue (the lanes
+                    // that reach this point together)
+                    const unsigned act = __activemask();
+                    const unsigned want = __ballot_sync(act, fits);
+                    unsigned slot = (unsigned)kQueue;
+                    if (want) {
+                        const int leader = __ffs(want) - 1;
+                        unsigned qb = 0;
+                        if (lane == leader) qb = atomicAdd(qcount, (unsigned)__popc(want));
+                        qb = __shfl_sync(act, qb, leader);
+                        if (fits) slot = qb + (unsigned)__popc(want & ((1u << lane) - 1u));
+                    }
                     if (slot < (unsigned)kQueue) {
                         q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
                         q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
