@@ -90,6 +90,34 @@ def test_sort_large_buckets_and_empty_cells(pic, oracle_mod):
     assert np.array_equal(gP, orc.P[0])
 
 
+@pytest.mark.parametrize("case", ["wide_supercell", "over_smem_stage"])
+def test_sort_order_kernel_paths(pic, oracle_mod, case):
+    """The per-supercell order kernel's other paths, bit-exact against the
+    oracle's stable sort: S = 8 (512 cells per supercell: the slot position
+    counted cell by cell instead of from slot tables) and 100 particles per
+    cell at S = 4 (6400 per supercell: more than the kernel stages in shared
+    memory, buckets ordered through global scratch)."""
+    from synth import Workload, gen_particles
+    from synth.configs import electron
+    if case == "wide_supercell":
+        wl = Workload("wide", 8, 8, 16, (electron(4, 0.05),), steps=1, sort_every=1, supercell=8)
+    else:
+        wl = Workload("full", 8, 8, 4, (electron(100, 0.05),), steps=1, sort_every=1, supercell=4)
+    P, ids = gen_particles(wl)[0]
+    perm = np.random.default_rng(11).permutation(P.shape[1])
+    P, ids = P[:, perm].copy(), ids[perm].copy()
+    orc = _oracle_for(oracle_mod, wl, [(P, ids)])
+    orc.sort()
+    sim = _sim(pic, wl)
+    sim.set_particles(0, P, ids)
+    gP, gids = sim.get_particles(0)
+    assert np.array_equal(gids, orc.ids[0])
+    assert np.array_equal(gP, orc.P[0])
+    sim.step(2)   # a re-sort of the pushed state; the particles stay valid and complete
+    gP2, gids2 = sim.get_particles(0)
+    assert np.array_equal(np.sort(gids2), np.sort(ids))
+
+
 # ---------------------------------------------------------------- fields (a7)
 
 def test_fdtd_random_fields_vs_oracle(pic, oracle_mod):
