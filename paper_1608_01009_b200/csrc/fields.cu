@@ -65,8 +65,11 @@ k_b_half(GridDev g, const double *__restrict__ EB, const double *Bin, double *Bo
 
 __global__ void __launch_bounds__(256)
 k_e_full(GridDev g, double *__restrict__ EB, const double *__restrict__ Bh, double *__restrict__ Jc,
-         double *__restrict__ Jn, double coefE, double coefJ)
+         double *__restrict__ Jn, double coefE, double coefJ, StepPrep prep)
 {
+    // the next step's J-tile scales (this step's particle kernels are done)
+    if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.y) == 0 && (int)threadIdx.x < prep.n_species)
+        step_prep_species(prep, threadIdx.x);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     const int k = blockIdx.z;
@@ -241,11 +244,12 @@ void launch_b_half(const GridDev &g, const double *EB, const double *Bin, double
     k_b_half<<<grid, bs, 0, st>>>(g, EB, Bin, Bout1, Bout2, 0.5 * g.c * g.dt, kbegin);
 }
 
-void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext, cudaStream_t st)
+void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext,
+                   const StepPrep &prep, cudaStream_t st)
 {
     const dim3 bs(32, 8, 1);
     k_e_full<<<field_grid(g, bs), bs, 0, st>>>(g, EB, Bh, Jcur, Jnext, g.c * g.dt,
-                                                4.0 * M_PI * g.dt);
+                                                4.0 * M_PI * g.dt, prep);
 }
 
 void launch_laser_coeffs(const GridDev &g, const double laser[6], int64_t *step, double *out, cudaStream_t st)

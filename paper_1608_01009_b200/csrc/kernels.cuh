@@ -7,6 +7,38 @@
 
 namespace pic {
 
+// per step: fixed-point J-tile scale per species from u2max_in, u2max_out = 0
+// (a stand-alone launch before the first step; then by the previous step's
+// k_e_full, which runs after that step's particle kernels)
+struct StepPrep {
+    int n_species;
+    double qw[4];
+    double c, dV;
+    const unsigned *u2max_in;   // the bound of the step that was pushed last
+    unsigned *u2max_out;        // reset for the next step's particle kernels
+    double *scale;              // [species][2]: 2^F, 2^-F
+};
+void launch_step_prep(const StepPrep &p, cudaStream_t st);
+
+// Every contribution to the J tile is bounded by |qw| c beta / (dx dy dz) *
+// 13/12 with beta <= 2 x the largest beta of the last step (from its max
+// |u|^2); 2^F maps that bound to < 2^46 (the fixed-point notes in push_tile.cu).
+__device__ __forceinline__ void step_prep_species(const StepPrep &p, int s)
+{
+    const double u2 = __longlong_as_double(((unsigned long long)p.u2max_in[s] << 32) | 0xffffffffull);
+    const double beta = fmax(1e-4, fmin(1.0, 2.0 * sqrt(u2 / (1.0 + u2))));
+    // constant indices only: a runtime index into the parameter struct would
+    // copy it to local memory in every thread of the calling kernel
+    double qw = p.qw[0];
+#pragma unroll
+    for (int t = 1; t < 4; ++t) qw = s == t ? p.qw[t] : qw;
+    const double wmax = fabs(qw) * p.c / p.dV * (13.0 / 12.0) * beta;
+    const int F = wmax > 0.0 ? min(1000, (int)floor(46.0 - log2(wmax))) : 1000;
+    p.scale[2 * s] = ldexp(1.0, F);
+    p.scale[2 * s + 1] = ldexp(1.0, -F);
+    p.u2max_out[s] = 0u;
+}
+
 // ---- fields.cu : Yee FDTD and ghost maintenance ----
 // Bout1 = Bin - (c dt/2) curl E (E of EB), and with Bout2 also Bout2 = Bout1 -
 // (c dt/2) curl E, on planes [kbegin, nz) (kbegin = -1 computes the lower z
@@ -16,7 +48,10 @@ void launch_b_half(const GridDev &g, const double *EB, const double *Bin, double
 // E += c dt curl Bh - 4 pi dt J (Bh = B^{n+1/2}) where J = sum of the ghost
 // images of Jcur (the fold); writes the folded J back into
 // Jcur's interior, stores E to its ghost images and zeroes every image of Jnext.
-void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext, cudaStream_t st);
+// With prep.n_species > 0 its first threads also run the next step's J-tile
+// scale preparation (launch_step_prep's work, after this step's particle kernels).
+void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext,
+                   const StepPrep &prep, cudaStream_t st);
 // Copies interior values of `ncomp` components to their ghost images.
 void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st);
 // NEXT-1 (open z): laser = {e0, omega, ramp, t0, pol_x, pol_y}.  Writes the
@@ -39,14 +74,6 @@ void launch_push_tail(const GridDev &g, const double *EB, double *J, const Parti
 // ---- push_tile.cu : fused supercell kernel ----
 bool tile_supported(int S);
 void tile_box(int S, int box[4]);   // TMA box of the E/B tile (x pitch, y, z, comps)
-// per step: fixed-point J-tile scale per species from u2max_in, u2max_out = 0
-struct StepPrep {
-    int n_species;
-    double qw[4];
-    double c, dV;
-};
-void launch_step_prep(const unsigned *u2max_in, unsigned *u2max_out, double *scale, const StepPrep &p,
-                      cudaStream_t st);
 // max |u|^2 of n particles -> *out (high 32 bits of the fp64 value)
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st);
 void configure_tile_kernels();

@@ -489,29 +489,18 @@ __global__ void __launch_bounds__(256) k_u2max(ParticlesDev P, int64_t n, unsign
     if ((threadIdx.x & 31) == 0 && hi) atomicMax(out, hi);
 }
 
-// Once per step, before the particle kernels: the fixed-point scale of each
+// Before the particle kernels of a step: the fixed-point scale of each
 // species' J tile from the previous step's speed bound, and the reset of this
-// step's bound.  Every contribution is bounded by |qw| c beta / (dx dy dz) *
-// 13/12 with beta <= 2 x the largest beta of the previous step (from its max
-// |u|^2); 2^F maps that bound to < 2^46 (see the fixed-point notes above).
-__global__ void k_step_prep(const unsigned *__restrict__ u2max_in, unsigned *__restrict__ u2max_out,
-                            double *__restrict__ scale, StepPrep p)
+// step's bound (step_prep_species).  A stand-alone launch only before the
+// first step after new particles; every step's k_e_full prepares the next.
+__global__ void k_step_prep(StepPrep p)
 {
-    const int s = threadIdx.x;
-    if (s >= p.n_species) return;
-    const double u2 = __longlong_as_double(((unsigned long long)u2max_in[s] << 32) | 0xffffffffull);
-    const double beta = fmax(1e-4, fmin(1.0, 2.0 * sqrt(u2 / (1.0 + u2))));
-    const double wmax = fabs(p.qw[s]) * p.c / p.dV * (13.0 / 12.0) * beta;
-    const int F = wmax > 0.0 ? min(1000, (int)floor(46.0 - log2(wmax))) : 1000;
-    scale[2 * s] = ldexp(1.0, F);
-    scale[2 * s + 1] = ldexp(1.0, -F);
-    u2max_out[s] = 0u;
+    if ((int)threadIdx.x < p.n_species) step_prep_species(p, threadIdx.x);
 }
 
-void launch_step_prep(const unsigned *u2max_in, unsigned *u2max_out, double *scale, const StepPrep &p,
-                      cudaStream_t st)
+void launch_step_prep(const StepPrep &p, cudaStream_t st)
 {
-    k_step_prep<<<1, 32, 0, st>>>(u2max_in, u2max_out, scale, p);
+    k_step_prep<<<1, 32, 0, st>>>(p);
 }
 
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st)

@@ -279,6 +279,7 @@ struct pic_ctx {
     double *EB = nullptr;
     double *Bh = nullptr;      // B^{n+1/2} for the next E update (bit-equal to a half step of EB's B)
     bool bh_stale = false;     // Bh must be recomputed from EB (after pic_set_fields / pic_laser_preload)
+    bool prep_ready = false;   // the next step's J-tile scales are prepared (by k_e_full)
     double *J[2] = {nullptr, nullptr};
     int jcur = 0;              // J buffer receiving the next deposit
     int jlast = 1;             // J buffer holding J^{n-1/2}
@@ -493,16 +494,8 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
             }
     }
     StageMark m(ctx, 1, profile);
-    // u^2 bounds: this step reads parity jcur (-> the J-tile scales), writes parity 1 - jcur
-    {
-        StepPrep p{};
-        p.n_species = (int)ctx->cfg.n_species;
-        for (int s = 0; s < p.n_species; ++s) p.qw[s] = ctx->cfg.q[s] * ctx->cfg.w[s];
-        p.c = g.c;
-        p.dV = g.dx * g.dy * g.dz;
-        launch_step_prep(ctx->u2max[jcur], ctx->u2max[1 - jcur], ctx->tile_scale, p, ctx->st);
-        ++launches;
-    }
+    // u^2 bounds: this step reads parity jcur (its J-tile scales were prepared by
+    // the previous step's k_e_full or by ensure_prep), writes parity 1 - jcur
     if (ctx->use_tile) {
         // species go in pairs: one launch walks both species of a supercell in
         // one particle loop, so its E/B tile load, J-tile zeroing and flush,
@@ -559,6 +552,30 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
     return launches;
 }
 
+// J-tile scale preparation from the u^2 bound of parity `from` (the step that
+// was pushed last), resetting the other parity for the next push
+StepPrep make_prep(const pic_ctx *ctx, int from)
+{
+    StepPrep p{};
+    p.n_species = (int)ctx->cfg.n_species;
+    for (int s = 0; s < p.n_species; ++s) p.qw[s] = ctx->cfg.q[s] * ctx->cfg.w[s];
+    p.c = ctx->L.g.c;
+    p.dV = ctx->L.g.dx * ctx->L.g.dy * ctx->L.g.dz;
+    p.u2max_in = ctx->u2max[from];
+    p.u2max_out = ctx->u2max[1 - from];
+    p.scale = ctx->tile_scale;
+    return p;
+}
+
+// before the first step after new particles: the stand-alone preparation
+void ensure_prep(pic_ctx *ctx)
+{
+    if (ctx->prep_ready) return;
+    launch_step_prep(make_prep(ctx, ctx->jcur), ctx->st);
+    ctx->launches += 1;
+    ctx->prep_ready = true;
+}
+
 int phase_fields_e(pic_ctx *ctx, int jcur, bool profile)
 {
     const GridDev &g = ctx->L.g;
@@ -578,7 +595,8 @@ int phase_fields_e(pic_ctx *ctx, int jcur, bool profile)
         launch_laser_coeffs(g, ctx->laser_par, ctx->dev_step, ctx->laser, ctx->st);
         ++launches;
     }
-    launch_e_full(g, ctx->EB, ctx->Bh, ctx->J[jcur], ctx->J[1 - jcur], ctx->st);
+    // + the next step's J-tile scales from this step's bound (parity 1 - jcur)
+    launch_e_full(g, ctx->EB, ctx->Bh, ctx->J[jcur], ctx->J[1 - jcur], make_prep(ctx, 1 - jcur), ctx->st);
     return launches + 1;
 }
 
@@ -945,6 +963,7 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
     sort_particles(g, Bs, ctx->A[species], ctx->dev_n + species, std::max<int64_t>(m, 1), ctx->sort,
                    ctx->sc_off[species], ctx->err, ctx->st, &launches);
     launch_u2max(ctx->A[species], m, ctx->u2max[ctx->jcur] + species, ctx->st);
+    ctx->prep_ready = false;
     ctx->launches += launches + 1;
     if (!ctx->slabs) {   // the device-side range check of the key pass
         unsigned h = 0;
@@ -1091,7 +1110,10 @@ int pic_step(pic_ctx *ctx, int64_t nsteps)
         if (rc != PIC_OK) return rc;
         ctx->ghosts_stale = false;
     }
-    if (nsteps > 0) refresh_bh(ctx);
+    if (nsteps > 0) {
+        refresh_bh(ctx);
+        ensure_prep(ctx);
+    }
     for (int64_t s = 0; s < nsteps; ++s) {
         const bool sort_now = K > 0 && (ctx->step_index % K) == 0;
         const int jc = ctx->jcur;
@@ -1139,7 +1161,10 @@ int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps)
         for (int r = 0; r < n; ++r) ctxs[r]->ghosts_stale = false;
     }
     if (nsteps > 0)
-        for (int r = 0; r < n; ++r) refresh_bh(ctxs[r]);
+        for (int r = 0; r < n; ++r) {
+            refresh_bh(ctxs[r]);
+            ensure_prep(ctxs[r]);
+        }
     for (int64_t s = 0; s < nsteps; ++s) {
         const int64_t K = ctxs[0]->cfg.sort_every;
         const bool sort_now = K > 0 && (ctxs[0]->step_index % K) == 0;
