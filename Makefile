@@ -1,6 +1,7 @@
 # Builds the product library (CUDA, sm_100a) and the CPU oracle (plain C).
 #   make            -> paper_1608_01009_b200/libpic.so  oracle/liboracle.so
 #   make sass       -> SASS dump of libpic.so into build/libpic.sass
+#   make checked    -> exp/libpic_checked.so with the internal index checks (-DPIC_CHECK)
 NVCC     ?= /usr/local/cuda/bin/nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NCCL_INC ?= $(shell python3 -c "import os,nvidia.nccl as m; print(os.path.join(list(m.__path__)[0],'include'))" 2>/dev/null || echo /usr/include)
@@ -23,10 +24,20 @@ $(PKG)/libpic.so: $(OBJ)
 oracle/liboracle.so: oracle/pic_oracle.c oracle/pic_oracle.h
 	gcc -std=gnu11 -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
 
+CHKOBJ   := $(patsubst $(PKG)/csrc/%.cu,build/chk/%.o,$(CSRC))
+
+build/chk/%.o: $(PKG)/csrc/%.cu $(CHDR)
+	@mkdir -p build/chk
+	$(NVCC) $(NVFLAGS) -DPIC_CHECK -c $< -o $@ 2> build/chk/$*.ptxas.log || (cat build/chk/$*.ptxas.log; false)
+
+checked: $(CHKOBJ)
+	@mkdir -p exp
+	$(NVCC) $(ARCH) -shared -cudart static -o exp/libpic_checked.so $(CHKOBJ) -ldl
+
 sass: $(PKG)/libpic.so
 	/usr/local/cuda/bin/cuobjdump -sass $< > build/libpic.sass
 
 clean:
 	rm -rf build $(PKG)/libpic.so oracle/liboracle.so
 
-.PHONY: all clean sass
+.PHONY: all clean sass checked

@@ -15,6 +15,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifdef PIC_CHECK
+#include <cstdio>
+#endif
+
 namespace pic {
 
 constexpr int kGhost = 2;   // G: CIC gather needs [-1, n], VB edges need [-1, n+1]
@@ -25,7 +29,27 @@ enum : unsigned {
     kErrNonFinite = 2u,
     kErrCapacity = 4u,
     kErrRange = 8u,
+    kErrCheck = 16u,   // an internal index check of a PIC_CHECK build failed
 };
+
+// Internal index checks of a debugging build (make CHECK=1 -> -DPIC_CHECK):
+// a failed check sets kErrCheck in the error word (the call then returns
+// PIC_ECUDA); compiled out otherwise.
+#ifdef PIC_CHECK
+#define PIC_DCHECK(cond, errp)                                                          \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            if (!(atomicOr((errp), (unsigned)::pic::kErrCheck) & ::pic::kErrCheck))     \
+                printf("PIC_CHECK failed: %s:%d block %d thread %d\n", __FILE__, __LINE__, \
+                       (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)), \
+                       (int)threadIdx.x);                                               \
+        }                                                                               \
+    } while (0)
+#else
+#define PIC_DCHECK(cond, errp) \
+    do {                       \
+    } while (0)
+#endif
 
 struct GridDev {
     int nx, ny, nz;          // local interior cells (nz = slab thickness)

@@ -98,9 +98,18 @@ template <class T>
 __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, int64_t gorigin,
                                             const GridDev &g, double p1x, double p1y, double p1z,
                                             double p2x, double p2y, double p2z, double kx,
-                                            double ky, double kz, double scale, bool fits)
+                                            double ky, double kz, double scale, bool fits,
+                                            unsigned *chk = nullptr)
 {
     constexpr int PX = T::JPX, PY = T::JPY, NJ = T::NJ;
+#ifdef PIC_CHECK   // the cell's 12 edges lie inside the J tile
+    if (chk) {
+        const int tz = jbase / PY, ty = (jbase % PY) / PX, tx = (jbase % PY) % PX;
+        PIC_DCHECK(jbase >= 0 && tx + 1 < T::TJ && ty + 1 < T::TJ && tz + 1 < T::TJ, chk);
+    }
+#else
+    (void)chk;
+#endif
     const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
     const double mx = 0.5 * (p1x + p2x), my = 0.5 * (p1y + p2y), mz = 0.5 * (p1z + p2z);
     const double fx = kx * Dx, fy = ky * Dy, fz = kz * Dz;
@@ -175,14 +184,15 @@ template <class T>
 __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *J, int64_t gorigin,
                                                   const GridDev &g, double a0, double a1,
                                                   double a2, double b0, double b1, double b2,
-                                                  double kx, double ky, double kz, double scale, bool fits)
+                                                  double kx, double ky, double kz, double scale, bool fits,
+                                                  unsigned *chk = nullptr)
 {
 #pragma unroll 1
     for (int it = 0; it < 3; ++it) {
         double e0, e1, e2, r1[3], r2[3];
         int ox, oy, oz;
         const bool more = vb_first_piece(a0, a1, a2, b0, b1, b2, e0, e1, e2, r1, r2, ox, oy, oz);
-        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale, fits);
+        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale, fits, chk);
         if (!more) break;
         jb += ox + T::JPX * oy + T::JPY * oz;
         a0 = r1[0]; a1 = r1[1]; a2 = r1[2];
@@ -328,6 +338,10 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
 #else
             const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
 #endif
+            // the 8 corners of every component lie inside the E/B tile
+            PIC_DCHECK(hx >= 0 && hy >= 0 && hz >= 0 && tx >= 0 && ty >= 0 && tz >= 0 && hx + 1 < T::TE &&
+                           hy + 1 < T::TE && hz + 1 < T::TE && tx + 1 < T::TE && ty + 1 < T::TE && tz + 1 < T::TE,
+                       err);
 #ifndef PIC_EXP_NOPUSH   // timing experiment only: no gather, no Boris
             const double ex = trilinear(eb + 0 * NE, hx + EPX * ty + EPY * tz, EPX, EPY, wx.fh, wy.f0, wz.f0);
             const double ey = trilinear(eb + 1 * NE, tx + EPX * hy + EPY * tz, EPX, EPY, wx.f0, wy.fh, wz.f0);
@@ -372,7 +386,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                     vb_first_piece(wx.f0, wy.f0, wz.f0, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
                 const bool fits = fits_tile(dxl, dyl, dzl, kx, ky, kz, scale);
                 deposit_seg<T>(jt, jbase, J, gorigin, g, wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx, ky, kz, scale,
-                               fits);
+                               fits, err);
                 if (more) {
                     // the rest of a face-crossing path is deposited after the particle
                     // loop, all queued paths together (keeps the loop convergent); the
@@ -397,7 +411,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                         qcell[slot] = (unsigned)jrem | (s1 ? 0x80000000u : 0u);
                     } else {
                         deposit_remainder<T>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0], r2[1],
-                                             r2[2], kx, ky, kz, scale, fits);
+                                             r2[2], kx, ky, kz, scale, fits, err);
                     }
                 }
 #endif
@@ -430,7 +444,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         const SpeciesDev &sp = (qc >> 31) ? ts.sp[NSP - 1] : ts.sp[0];
         deposit_remainder<T>(jt, (int)(qc & 0x7fffffffu), J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
                              q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], sp.kx, sp.ky, sp.kz, scale,
-                             true);
+                             true, err);
     }
     const int nf = min(*fqcount, (unsigned)kFQueue);
     for (int e = tid; e < nf; e += NT) {

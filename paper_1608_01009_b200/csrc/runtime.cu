@@ -710,6 +710,7 @@ int check_device_error(pic_ctx *ctx)
     if (h & kErrDisplacement) return fail(ctx, PIC_EDISPLACEMENT, "displacement >= 1 cell");
     if (h & kErrRange) return fail(ctx, PIC_EINVAL, "particle position outside the domain / slab");
     if (h & kErrCapacity) return fail(ctx, PIC_ECAPACITY, "device capacity exceeded (particles or migration)");
+    if (h & kErrCheck) return fail(ctx, PIC_ECUDA, "internal index check failed (PIC_CHECK build)");
     return PIC_OK;
 }
 
