@@ -447,6 +447,35 @@ def run_ours(args, wl, rank, world, local):
         dist.destroy_process_group()
 
 
+def cpu_baseline_all(path, seconds):
+    """The cpu_baseline leg over every workload (no GPU): the oracle as it
+    stands, one thread, on bounded samples (SURVEY.md sec. 8d oracle timing);
+    C1, C2 and FROZEN whole, the larger ones a particle sample over the whole
+    grid.  Writes a JSON file and prints one line per workload."""
+    import platform
+    from synth import gen_particles, get_config
+    rows = []
+    for name in ("C1", "C2", "C3", "C4", "C5_1g", "FROZEN"):
+        wl = get_config(name)
+        parts = gen_particles(wl)
+        v, ns, nsteps, dt = oracle_sample_rate(wl, parts, target_s=seconds)
+        rows.append({"workload": name, "particles": wl.n_particles, "sample_particles": ns, "steps": nsteps,
+                     "seconds": dt, "updates_per_s": v, "ns_per_particle_step": 1e9 / v,
+                     "whole": ns == wl.n_particles})
+        print(json.dumps(rows[-1]), flush=True)
+    host = {"cpu": platform.processor() or platform.machine(), "nproc": os.cpu_count(), "threads_used": 1}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    host["cpu"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    with open(path, "w") as f:
+        json.dump({"host": host, "target_s": seconds, "rows": rows}, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -461,7 +490,12 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=50_000)
     ap.add_argument("--supercell", type=int, default=None, help="override S (tools/sweep.py)")
     ap.add_argument("--sort-every", type=int, default=None, help="override K (tools/sweep.py)")
+    ap.add_argument("--cpu-baseline-all", default=None, metavar="OUT.json",
+                    help="only time the oracle (cpu_baseline leg) on every workload; no GPU")
     args = ap.parse_args()
+    if args.cpu_baseline_all:
+        cpu_baseline_all(args.cpu_baseline_all, args.cpu_seconds)
+        return
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
     rank, world, local = dist_env()
     from synth import get_config
