@@ -439,12 +439,45 @@ def test_supercell_two_tile_kernel(pic, oracle_mod):
 
 
 def test_dense_supercell_global_path(pic, oracle_mod):
-    """A supercell holding more particles than the fixed-point tile counters
-    allow (> 16383) is pushed through the global path; results unchanged."""
+    """Uniformly dense supercells (19200 particles each, more than the
+    fixed-point tile counters allow in one CTA): the launch splits each over
+    several CTAs (mean > 8192 per supercell), each within the counter bound;
+    results unchanged."""
     from synth import Workload
     from synth.configs import electron
     wl = Workload("dense", 8, 8, 8, (electron(300, 0.05),), steps=2, sort_every=2, supercell=4)
     _run_parity(pic, oracle_mod, wl, 2, teacher_forced=True, tol=1e-12)
+
+
+def test_one_overdense_supercell_takes_the_global_path(pic, oracle_mod):
+    """One supercell holding 17000 particles while the mean stays low (no
+    split): its CTA exceeds the fixed-point counter bound (16383), so every
+    one of its particles is pushed and deposited by the global fp64 path
+    (outside-tile queue, then inline once the queue is full) while the other
+    CTAs use the tile; per step against the oracle."""
+    from synth import Workload, gen_particles
+    from synth.configs import electron
+    wl = Workload("overdense", 8, 8, 8, (electron(2, 0.05),), steps=3, sort_every=2, supercell=4)
+    P0, i0 = gen_particles(wl)[0]
+    rng = np.random.default_rng(31)
+    m = 17000
+    Pd = np.empty((6, m))
+    Pd[:3] = rng.random((3, m)) * 4.0          # supercell (0, 0, 0): cells [0, 4)^3
+    Pd[3:] = rng.standard_normal((3, m)) * 0.05
+    P = np.concatenate([P0, Pd], axis=1)
+    ids = np.arange(P.shape[1], dtype=np.uint64) + 7
+    orc = _oracle_for(oracle_mod, wl, [(P, ids)])
+    sim = _sim(pic, wl, counts=[P.shape[1]])
+    L = _L(wl)
+    for step in range(3):
+        sim.set_fields(orc.F[:6].copy())
+        sim.set_particles(0, orc.P[0], orc.ids[0])
+        orc.step(1)
+        sim.step(1)
+        errs = field_errs(sim.get_fields(), orc.F)
+        gP, gi = sim.get_particles(0)
+        errs += list(compare_state(gP, gi, orc.P[0], orc.ids[0], L))
+        assert max(errs) <= TOL_STEP, (step, errs)
 
 
 def test_particles_on_faces_and_corners(pic, oracle_mod):
