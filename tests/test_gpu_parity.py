@@ -221,6 +221,23 @@ def test_nonunit_cells_and_strong_fields(pic, oracle_mod):
     _run_parity(pic, oracle_mod, wl, 6, teacher_forced=True, fields=F6)
 
 
+def test_sudden_acceleration_takes_the_fp64_deposit(pic, oracle_mod):
+    """A cold plasma (sigma 1e-4) put into strong fields: in the first step
+    every particle speeds up far beyond the 2x headroom of the fixed-point
+    scale set from the previous speed bound, so its segments fail the range
+    check and go to the fp64 global J (deposit_seg's fallback); the next
+    steps use the tile again with the new bound.  Free running against the
+    oracle.  (Round 1 checked with a debug build that flags the fallback that
+    this case takes it and C1 does not.)"""
+    from synth import get_config
+    from synth.configs import electron, proton
+    wl = get_config("T_two_species").with_(species=(electron(3, 1e-4), proton(3, 1e-4)), supercell=4)
+    rng = np.random.default_rng(12)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.2
+    F6[0] += 1.5                       # a uniform Ex on top: |du| ~ 0.4 per step
+    _run_parity(pic, oracle_mod, wl, 4, teacher_forced=False, fields=F6, tol=1e-11)
+
+
 def test_tile_fallback_after_long_drift(pic, oracle_mod):
     """No re-sort for 30 steps at sigma 0.3: particles drift beyond the
     tile halo and take the global fallback path of the fused kernel."""
