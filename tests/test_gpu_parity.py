@@ -238,6 +238,17 @@ def test_sudden_acceleration_takes_the_fp64_deposit(pic, oracle_mod):
     _run_parity(pic, oracle_mod, wl, 4, teacher_forced=False, fields=F6, tol=1e-11)
 
 
+def test_remainder_queue_overflow(pic, oracle_mod):
+    """6400 hot particles per supercell (100 ppc, sigma 0.5): about a third of
+    them cross a cell face every step, far more than the CTA's remainder
+    queue holds (160), so the overflowing paths deposit their rest inline;
+    free running against the oracle."""
+    from synth import Workload
+    from synth.configs import electron
+    wl = Workload("hot", 8, 8, 8, (electron(100, 0.5),), steps=4, sort_every=2, supercell=4)
+    _run_parity(pic, oracle_mod, wl, 4, teacher_forced=False, tol=1e-11)
+
+
 def test_tile_fallback_after_long_drift(pic, oracle_mod):
     """No re-sort for 30 steps at sigma 0.3: particles drift beyond the
     tile halo and take the global fallback path of the fused kernel."""
