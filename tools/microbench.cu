@@ -71,6 +71,38 @@ __global__ void k_copy(const double4 *__restrict__ a, double4 *__restrict__ b, i
         b[i] = a[i];
 }
 
+// dependent-chain latencies (one thread; cycles per operation from clock64)
+__global__ void k_lat(long long *cyc, double *sink, int n, double a, double b)
+{
+    __shared__ double sh[1024];
+    __shared__ unsigned su[64];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = (double)((i * 7 + 1) & 1023);
+    if (threadIdx.x < 64) su[threadIdx.x] = 0;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double x = a;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) x = fma(x, a, b);          // DFMA chain
+    long long t1 = clock64();
+    for (int i = 0; i < n; ++i) x = x + b;                 // DADD chain
+    long long t2 = clock64();
+    for (int i = 0; i < n; ++i) {                          // MUFU.RSQ64H chain
+        double r;
+        asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x + 1.0));
+        x = r;
+    }
+    long long t3 = clock64();
+    int idx = 1;
+    for (int i = 0; i < n; ++i) idx = (int)sh[idx];        // LDS.64 + F2I chain
+    long long t4 = clock64();
+    unsigned v = 0;
+    for (int i = 0; i < n; ++i) v = atomicAdd(&su[v & 63], 1u);   // ATOMS with return chain
+    long long t5 = clock64();
+    cyc[0] = (t1 - t0) / n; cyc[1] = (t2 - t1) / n; cyc[2] = (t3 - t2) / n; cyc[3] = (t4 - t3) / n;
+    cyc[4] = (t5 - t4) / n;
+    sink[0] = x + idx + v;
+}
+
 int main()
 {
     cudaDeviceProp prop;
@@ -159,6 +191,17 @@ int main()
             if (ms < best) best = ms;
         }
         printf(", \"copy_gbs\": %.1f", 2.0 * bytes / (best * 1e-3) / 1e9);
+    }
+    {   // latencies
+        long long *cyc;
+        CK(cudaMalloc(&cyc, 8 * sizeof(long long)));
+        k_lat<<<1, 64>>>(cyc, d, 256, 1.0000001, 1e-9);
+        k_lat<<<1, 64>>>(cyc, d, 4096, 1.0000001, 1e-9);
+        CK(cudaDeviceSynchronize());
+        long long h[5];
+        CK(cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost));
+        printf(", \"lat_cycles\": {\"dfma\": %lld, \"dadd\": %lld, \"mufu_rsq64h\": %lld, \"lds64_f2i\": %lld, "
+               "\"atoms_ret\": %lld}", h[0], h[1], h[2], h[3], h[4]);
     }
     printf("}\n");
     return 0;
