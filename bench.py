@@ -7,9 +7,11 @@ ns/particle/step, % HBM roofline).
 
 A "step" is one PIC time step of the whole hot path (SURVEY.md sec. 8a:
 sort every K steps, fused gather/push/deposit, J fold, Yee update) over the
-workload's synthetic particles.  At N=1 the default workload is C2 =
-BASELINE.json configs[1] (40^3, 50 e/cell = 3.2M particles; its particle
-state, 180 MB, is larger than the 126 MB L2, so no explicit L2 flush).
+workload's synthetic particles.  At N=1 the default workload is C3 =
+BASELINE.json configs[2], the largest single-GPU configuration (128^3, 25 e +
+25 p per cell = 104.9M particles in one fused launch per step; its particle
+state, 5.9 GB, is far larger than the 126 MB L2, so no explicit L2 flush);
+at N>1 it is C4 (weak scaling).  C1, C2, FROZEN and C5_1g via --workload.
 
 --impl reference times the CPU oracle (oracle/, plain serial C) on the same
 workload: each step pushes a fixed bounded sample of the particles through
@@ -47,9 +49,24 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-# fp64 work of one particle update: 336 flop (FMA = 2), the paper's VTune
-# count (PAPER.md:190 with Table 6 times)
-FLOP_PER_UPDATE = 336.0
+# fp64 work of one particle update as the paper counts it: 336 flop (FMA = 2),
+# its VTune figure (PAPER.md:190 with Table 6 times) -- a
+# different code; reported beside this kernel's own ncu-counted figure
+PAPER_FLOP_PER_UPDATE = 336.0
+
+
+def load_ncu_counts(workload):
+    """Per-launch ncu counts of the fused particle kernel for a workload
+    (profiles/ncu_particle_traffic.json): DRAM bytes and the executed fp64
+    thread instructions (DFMA counted as 2 flop), with the commit and the
+    capture they came from.  ncu cannot run inside the timed bench, so these
+    are the last capture's numbers, labelled as such."""
+    p = os.path.join(ROOT, "profiles", "ncu_particle_traffic.json")
+    if not os.path.exists(p):
+        return {}, None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(workload, {}), d.get("_source")
 
 
 def load_fp64_peak():
@@ -224,17 +241,56 @@ def oracle_sample_rate(wl, parts, target_s=10.0, max_particles=None):
     return n_sample * steps / dt, n_sample, steps, dt
 
 
+def host_info():
+    """The host the oracle ran on: logical CPUs and the CPU model."""
+    import platform
+    host = {"nproc": os.cpu_count(), "cpu": platform.processor() or platform.machine(), "threads_used": 1}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    host["cpu"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return host
+
+
+def fp64_roof(rate_per_gpu, flop_upd, ncu, peak, peak_src):
+    """The FP64 roof of SURVEY.md sec. 8d from this kernel's own counted work
+    per update (ncu opcode mix of the captured launch, null if none), with
+    the paper's 336 flop/update alongside as a labelled figure."""
+    out = {"peak_tflops": peak, "peak_source": peak_src,
+           "paper_flop_per_update": PAPER_FLOP_PER_UPDATE,
+           "paper_frac": rate_per_gpu * PAPER_FLOP_PER_UPDATE / 1e12 / peak}
+    if flop_upd:
+        out.update({"flop_per_update": flop_upd,
+                    "flop_source": f"ncu sm__sass_thread_inst_executed_op_d{{fma,add,mul}}_pred_on "
+                                   f"(DFMA = 2 flop) of the particle kernel at commit {ncu.get('commit', '?')}; "
+                                   f"the sort and field kernels' few fp64 operations are not included",
+                    "achieved_tflops": rate_per_gpu * flop_upd / 1e12,
+                    "frac": rate_per_gpu * flop_upd / 1e12 / peak})
+    else:
+        out.update({"flop_per_update": None, "achieved_tflops": None, "frac": None})
+    return out
+
+
 # ------------------------------------------------------------------ arms
 
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return
     from synth import gen_particles
-    parts = gen_particles(wl)
+    n_sample = args.ref_sample
+    # a bounded sample: generate only the first z planes that hold it (the
+    # same distribution as the whole workload; C3 would be 105M particles)
+    ppc = sum(s.ppc for s in wl.species)
+    z0 = wl.plasma_z[0] if wl.plasma_z else 0
+    planes = min(wl.nz - z0, max(1, -(-n_sample // (ppc * wl.nx * wl.ny))))
+    parts = gen_particles(wl, z_lo=z0, z_hi=z0 + planes)
     from oracle import oracle as O
     O.build()
     g = oracle_grid(O, wl)
-    n_sample = args.ref_sample
     sub = []
     for P, ids in parts:
         k = min(P.shape[1], max(1, n_sample // len(parts)))
@@ -258,7 +314,8 @@ def run_reference(args, wl, rank, world):
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"first {ns} particles of {wl.name} (of {wl.n_particles}) "
                                    f"through full oracle steps (fields on the whole grid), "
-                                   f"single thread"},
+                                   f"single thread",
+                         "host": host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -363,13 +420,13 @@ def run_ours(args, wl, rank, world, local):
     peak, peak_src = load_peaks()
     fp64_peak, fp64_src = load_fp64_peak()
     n_cells_local = wl.nx * wl.ny * (slab[1] - slab[0])
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_particle_traffic.json")
-    if os.path.exists(tp):   # ncu dram read + write of one launch, per workload
-        try:
-            traffic = json.load(open(tp)).get(wl.name, {}).get("bytes_per_launch")
-        except Exception:
-            pass
+    ncu, ncu_src = load_ncu_counts(wl.name)
+    traffic = ncu.get("bytes_per_launch")
+    traffic_src = (f"ncu --set full of one launch at commit {ncu.get('commit', '?')} "
+                   f"({ncu.get('capture', ncu_src)}), not measured in this run") if traffic else None
+    # this kernel's own fp64 work per update (ncu opcode counts of the captured
+    # launch: 2 DFMA + DADD + DMUL thread instructions over its particles)
+    flop_upd = ncu.get("fp64_flop_per_update")
     step_ms_prof = (st["sort"] + st["particle"] + st["field"] + st["exchange"]) / args.steps
 
     # ---------------- e2e through the C ABI with host buffers
@@ -404,7 +461,8 @@ def run_ours(args, wl, rank, world, local):
                                                max_particles=args.cpu_max_particles)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{nsteps} oracle step(s) over {ns} of {wl.n_particles} particles of "
-                         f"{wl.name} (whole grid), {dt:.1f} s, single thread"}
+                         f"{wl.name} (whole grid), {dt:.1f} s, single thread",
+               "host": host_info()}
 
     if rank == 0:
         line = {
@@ -418,7 +476,7 @@ def run_ours(args, wl, rank, world, local):
             "data": "synthetic (seeded numpy PCG64, DESIGN.md sec. 6)",
             "config": wl_config(wl, world, split),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "particle (gather+Boris+VB deposit)",
                          "alg_bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": per_launch_ms, "peak_source": peak_src,
@@ -433,9 +491,7 @@ def run_ours(args, wl, rank, world, local):
                                              + n_cells_local * 120.0)
                          / (t_ms * 1e-3 / args.steps) / 1e9 / peak,
                          # the second roof (report both fractions)
-                         "fp64": {"achieved_tflops": value / world * FLOP_PER_UPDATE / 1e12,
-                                  "peak_tflops": fp64_peak, "frac": value / world * FLOP_PER_UPDATE / 1e12 / fp64_peak,
-                                  "flop_per_update": FLOP_PER_UPDATE, "peak_source": fp64_src}},
+                         "fp64": fp64_roof(value / world, flop_upd, ncu, fp64_peak, fp64_src)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -463,15 +519,7 @@ def cpu_baseline_all(path, seconds):
                      "seconds": dt, "updates_per_s": v, "ns_per_particle_step": 1e9 / v,
                      "whole": ns == wl.n_particles})
         print(json.dumps(rows[-1]), flush=True)
-    host = {"cpu": platform.processor() or platform.machine(), "nproc": os.cpu_count(), "threads_used": 1}
-    try:
-        with open("/proc/cpuinfo") as f:
-            for ln in f:
-                if ln.startswith("model name"):
-                    host["cpu"] = ln.split(":", 1)[1].strip()
-                    break
-    except OSError:
-        pass
+    host = host_info()
     with open(path, "w") as f:
         json.dump({"host": host, "target_s": seconds, "rows": rows}, f, indent=1)
 
@@ -499,7 +547,9 @@ def main():
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
     rank, world, local = dist_env()
     from synth import get_config
-    name = args.workload or ("C2" if world == 1 else "C4")
+    # N = 1: the largest single-GPU configuration (BASELINE.json configs[2]);
+    # N > 1: the weak-scaling slab run (configs[3])
+    name = args.workload or ("C3" if world == 1 else "C4")
     wl = get_config(name).for_ranks(world)
     if args.supercell:
         wl = wl.with_(supercell=args.supercell)

@@ -162,7 +162,9 @@ Layout make_layout(const pic_config *c)
             o = align_up(o + sizeof(double) * 3 * 2 * (size_t)g.X * g.Y);
         }
     }
-    const size_t capm = (size_t)std::max<int64_t>(L.cap_max, 1);
+    // +1: compact_live scans n + 1 entries (k_live_flags writes flag[n] into
+    // perm_tmp, k_scan_add writes perm[n])
+    const size_t capm = (size_t)std::max<int64_t>(L.cap_max, 1) + 1;
     L.off_key = o; o = align_up(o + 4 * capm);
     L.off_slot = o; o = align_up(o + 4 * capm);
     L.off_perm_tmp = o; o = align_up(o + 4 * capm);
@@ -217,8 +219,10 @@ const char *err_names(int code)
     }
 }
 
-// ---- NCCL, loaded at run time (only z-slab runs need it): the copy torch
-// already loaded if any, else the torch wheel's, else the system's ----
+// ---- NCCL, loaded at run time (only z-slab runs need it): the copy already
+// loaded into the process (torch's, when torch.distributed initialised NCCL),
+// else $PIC_NCCL_LIB (the Python binding points it at the torch wheel's
+// nvidia/nccl/lib/libnccl.so.2), else the loader's libnccl.so.2 ----
 struct NcclApi {
     void *h = nullptr;
     ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
@@ -237,12 +241,11 @@ NcclApi *nccl_api()
     static bool tried = false;
     if (tried) return api.h ? &api : nullptr;
     tried = true;
-    const char *names[] = {"libnccl.so.2",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
-                           "libnccl.so"};
     void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    for (const char *n : names)
-        if (!h) h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    const char *env = std::getenv("PIC_NCCL_LIB");
+    if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return nullptr;
     api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");

@@ -95,10 +95,28 @@ class PicError(RuntimeError):
 _lib = None
 
 
+def _nccl_hint():
+    """Point libpic's run-time NCCL loader (PIC_NCCL_LIB, runtime.cu nccl_api)
+    at the torch wheel's libnccl.so.2 unless the caller set it: z-slab runs
+    then use the same NCCL build as torch.distributed."""
+    if os.environ.get("PIC_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl as m
+        for d in m.__path__:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["PIC_NCCL_LIB"] = cand
+                return
+    except ImportError:
+        pass
+
+
 def lib():
     """Load libpic.so (raises if it was not built -- there is no fallback)."""
     global _lib
     if _lib is None:
+        _nccl_hint()
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build())")
         L = C.CDLL(LIB_PATH)

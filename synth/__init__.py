@@ -6,7 +6,7 @@ none of the PIC method's arithmetic (no gather, push, deposit or field
 update), and imports neither oracle/ nor paper_1608_01009_b200/.
 """
 from .configs import CONFIGS, Workload, SpeciesSpec, get_config, dt_courant
-from .gen import gen_particles, gen_species
+from .gen import gen_fields, gen_particles, gen_species
 
 __all__ = ["CONFIGS", "Workload", "SpeciesSpec", "get_config", "dt_courant",
-           "gen_particles", "gen_species"]
+           "gen_fields", "gen_particles", "gen_species"]

@@ -71,3 +71,15 @@ def gen_particles(wl: Workload, seed: int | None = None, rank: int | None = None
             pos = out[sp.colocate_with][0][:3]
         out.append(gen_species(wl, s, rng, z_lo, z_hi, positions=pos, id_base=base))
     return out
+
+
+def gen_fields(wl: Workload, seed: int = 7, e_sigma: float = 0.01, b_sigma: float = 0.1):
+    """Seeded synthetic E^0, B^0 for parity slices: every node value of
+    Ex,Ey,Ez ~ N(0, e_sigma), Bx,By,Bz ~ N(0, b_sigma) (numpy PCG64(seed)),
+    shape (6, nz, ny, nx), x fastest.  Random numbers only -- no method
+    arithmetic -- so the same array feeds the oracle and the GPU."""
+    rng = _rng(seed, None)
+    F = np.empty((6, wl.nz, wl.ny, wl.nx), dtype=np.float64)
+    F[:3] = rng.normal(0.0, e_sigma, (3, wl.nz, wl.ny, wl.nx))
+    F[3:] = rng.normal(0.0, b_sigma, (3, wl.nz, wl.ny, wl.nx))
+    return F

@@ -1,5 +1,5 @@
 """The bench.py contract pieces that run without a GPU: the reference arm's
-JSON line (the oracle on a bounded C2 sample) and the host helpers the
+JSON line (the oracle on a bounded sample of the default workload, C3) and the host helpers the
 GPU arm's line is built from (slab split, occupied cells, peaks)."""
 import json
 import os
@@ -23,7 +23,8 @@ def test_reference_arm_json_line():
         assert key in line, key
     assert line["impl"] == "reference" and line["n_gpus"] == 1 and line["steps"] == 2
     assert line["value"] > 0 and line["higher_is_better"] is True and line["dtype"] == "f64"
-    assert line["config"]["workload"] == "C2"
+    assert line["config"]["workload"] == "C3"   # the N = 1 default: largest single-GPU config
+    assert line["cpu_baseline"]["host"]["nproc"] >= 1
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
@@ -45,6 +46,10 @@ def test_host_helpers():
     assert peak > 1000 and isinstance(src, str)
     tf, tsrc = bench.load_fp64_peak()
     assert 10 < tf < 100 and isinstance(tsrc, str)
+    roof = bench.fp64_roof(20e9, None, {}, tf, tsrc)
+    assert roof["frac"] is None and roof["paper_flop_per_update"] == 336.0
+    roof = bench.fp64_roof(20e9, 250.0, {"commit": "abc"}, tf, tsrc)
+    assert roof["frac"] == pytest.approx(20e9 * 250.0 / 1e12 / tf)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])

@@ -1,0 +1,106 @@
+"""Whole-state GPU-vs-oracle parity at the BASELINE.json sizes (SURVEY.md
+sec. 8c gate: "<= 1e-12 per step on x, u, E, B, J ... a 2-step C2 slice";
+VERDICT r01 next #2).  Both sides start from the same synthetic seeded state
+(synth.gen_particles + synth.gen_fields: thermal particles and random E, B
+so the gather and the rotation are exercised) and run in the bench launch
+configuration (graphs, the fused two-species kernel, K = 20).  x and u are
+compared by particle id (positions by minimum image), E, B and J element by
+element, each array against its own maximum (reading R17); the measured
+per-array errors are printed (run with -s) so the fixed-point J tile's
+margin at production sizes is on record."""
+import time
+
+import numpy as np
+import pytest
+
+from tests.helpers import compare_state, field_errs
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-12
+NAMES = ("Ex", "Ey", "Ez", "Bx", "By", "Bz", "Jx", "Jy", "Jz")
+
+
+@pytest.fixture(scope="module")
+def pic():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1608_01009_b200 as P
+    P.lib()
+    return P
+
+
+def _oracle(O, wl, parts, F6):
+    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every)
+    return O.Oracle(g, particles=parts, fields=F6)
+
+
+def _errors(sim, orc, wl):
+    L = (wl.nx * wl.dx, wl.ny * wl.dy, wl.nz * wl.dz)
+    G = sim.get_fields()
+    errs = dict(zip(NAMES, field_errs(G, orc.F)))
+    del G
+    for s in range(len(wl.species)):
+        gP, gi = sim.get_particles(s)
+        pe, ue = compare_state(gP, gi, orc.P[s], orc.ids[s], L)
+        errs[f"x{s}"], errs[f"u{s}"] = pe, ue
+    return errs
+
+
+def _report(tag, step, errs):
+    print(f"{tag} step {step}: " + " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
+
+
+def test_c2_whole_state_slices(pic, oracle_mod):
+    """C2 (40^3, 3.2M electrons, K = 20): steps 1 and 2 from the common
+    state (step 0 is a sort step) at <= 1e-12 per array; the run continues
+    free to step 21 (drift out of the sorted order and out of the tiles,
+    the re-sort at step 20) and is compared again at steps 20 and 21."""
+    from synth import gen_fields, gen_particles, get_config
+    wl = get_config("C2")
+    parts = gen_particles(wl)
+    F6 = gen_fields(wl)
+    orc = _oracle(oracle_mod, wl, [(p.copy(), i.copy()) for p, i in parts], F6)
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    sim.set_fields(F6)
+    del parts
+    worst = {}
+    t0 = time.perf_counter()
+    for step in range(1, 22):
+        orc.step(1)
+        sim.step(1)
+        if step in (1, 2, 20, 21):
+            errs = _errors(sim, orc, wl)
+            _report("C2", step, errs)
+            worst[step] = max(errs.values())
+    print(f"C2 oracle + compare {time.perf_counter() - t0:.1f} s", flush=True)
+    assert worst[1] <= TOL_STEP and worst[2] <= TOL_STEP, worst
+    # free running from step 2 on (north_star: 1e-9 after 100 steps)
+    assert worst[20] <= 1e-11 and worst[21] <= 1e-11, worst
+
+
+def test_c3_whole_state_one_step(pic, oracle_mod):
+    """C3 (128^3, 52.4M electrons + 52.4M protons in ONE fused launch, the
+    merged fixed-point J tile at the electron quantum): one step from the
+    common state (a sort step) at <= 1e-12 per array."""
+    from synth import gen_fields, gen_particles, get_config
+    wl = get_config("C3")
+    parts = gen_particles(wl)
+    F6 = gen_fields(wl)
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    sim.set_fields(F6)
+    sim.step(1)
+    orc = _oracle(oracle_mod, wl, parts, F6)   # the oracle copies its inputs
+    del parts
+    t0 = time.perf_counter()
+    orc.step(1)
+    print(f"C3 oracle step {time.perf_counter() - t0:.1f} s", flush=True)
+    errs = _errors(sim, orc, wl)
+    _report("C3", 1, errs)
+    assert max(errs.values()) <= TOL_STEP, errs

@@ -38,20 +38,35 @@ def _L(wl):
     return (wl.nx * wl.dx, wl.ny * wl.dy, wl.nz * wl.dz)
 
 
-def field_errs_grouped(G, F):
-    """Reading R17 for the laser runs: the x-polarised wave dominates E and B
-    by up to 12 orders of magnitude over the plasma's response in the other
-    components (whose per-array maxima are then rounding noise), so E and B
-    errors are relative to max |E, B| over all six components, J errors to
-    max |J| over its three."""
+# components the x-polarised wave along z drives (Ex, By), the longitudinal
+# charge-separation field Ez and the currents Jx, Jz: compared per array
+PHYSICAL = (0, 2, 4, 6, 8)
+# Ey, Bx, Bz, Jy vanish by the symmetry of the wave (x-polarised, uniform in
+# x and y) and carry only the particles' shot noise: per array too, but the
+# denominator is floored at 1e-4 of the group maximum (max |E, B| for the
+# fields, max |J| for the currents) so that a component that is pure
+# rounding noise of the others is not divided by itself
+SYMMETRY_ZERO = (1, 3, 5, 7)
+FLOOR = 1e-4
+
+
+def open_field_errs(G, F):
+    """Reading R17 per array (max |G - F| / max |F| for every component),
+    with the SYMMETRY_ZERO floor above."""
     se = max(np.abs(F[:6]).max(), 1e-300)
     sj = max(np.abs(F[6:]).max(), 1e-300)
-    return [float(np.abs(G[c] - F[c]).max() / (se if c < 6 else sj)) for c in range(9)]
+    errs = []
+    for c in range(9):
+        den = max(np.abs(F[c]).max(), 1e-300)
+        if c in SYMMETRY_ZERO:
+            den = max(den, FLOOR * (se if c < 6 else sj))
+        errs.append(float(np.abs(G[c] - F[c]).max() / den))
+    return errs
 
 
 def _check(sim, orc, wl, tol, what):
     G = sim.get_fields()
-    errs = field_errs_grouped(G, orc.F)
+    errs = open_field_errs(G, orc.F)
     for s in range(len(wl.species)):
         gP, gi = sim.get_particles(s)
         errs += list(compare_state(gP, gi, orc.P[s], orc.ids[s], _L(wl)))
@@ -73,13 +88,13 @@ def test_vacuum_laser_injection_and_mur(pic, oracle_mod):
     sim = pic.simulation_from_workload(wl, counts=[1])
     sim.laser_preload()
     G = sim.get_fields()
-    assert max(field_errs_grouped(G, orc.F)[:6]) <= 1e-15
+    assert max(open_field_errs(G, orc.F)[:6]) <= 1e-15
     for n in range(150):
         orc.step(1)
         sim.step(1)
         if n % 10 == 9:
             G = sim.get_fields()
-            assert max(field_errs_grouped(G, orc.F)) <= TOL_STEP, n
+            assert max(open_field_errs(G, orc.F)) <= TOL_STEP, n
     assert np.abs(orc.F[0, -1]).max() > 0.1 * lz["e0"]   # the wave did reach the top face
 
 
@@ -212,7 +227,7 @@ def test_open_unequal_slabs_match_single_domain_oracle(pic, oracle_mod, split):
         orc.step(1)
         pic.step_group(sims, 1)
         G = np.concatenate([s.get_fields() for s in sims], axis=1)
-        errs = field_errs_grouped(G, orc.F)
+        errs = open_field_errs(G, orc.F)
         for s in range(2):
             Ps, Is = zip(*[sim.get_particles(s) for sim in sims])
             errs += list(compare_state(np.concatenate(Ps, axis=1), np.concatenate(Is),
