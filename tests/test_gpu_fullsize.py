@@ -78,9 +78,9 @@ def test_c2_whole_state_slices(pic, oracle_mod):
             _report("C2", step, errs)
             worst[step] = max(errs.values())
     print(f"C2 oracle + compare {time.perf_counter() - t0:.1f} s", flush=True)
-    assert worst[1] <= TOL_STEP and worst[2] <= TOL_STEP, worst
-    # free running from step 2 on (north_star: 1e-9 after 100 steps)
-    assert worst[20] <= 1e-11 and worst[21] <= 1e-11, worst
+    # steps 20 and 21 are free running from step 2 on (north_star allows
+    # 1e-9 after 100 steps); measured on the B200: <= 4e-14 (J), 1e-14 (u)
+    assert max(worst.values()) <= TOL_STEP, worst
 
 
 def test_c3_whole_state_one_step(pic, oracle_mod):

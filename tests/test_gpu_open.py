@@ -42,12 +42,19 @@ def _L(wl):
 # charge-separation field Ez and the currents Jx, Jz: compared per array
 PHYSICAL = (0, 2, 4, 6, 8)
 # Ey, Bx, Bz, Jy vanish by the symmetry of the wave (x-polarised, uniform in
-# x and y) and carry only the particles' shot noise: per array too, but the
-# denominator is floored at 1e-4 of the group maximum (max |E, B| for the
-# fields, max |J| for the currents) so that a component that is pure
-# rounding noise of the others is not divided by itself
+# x and y) and carry only the particles' shot noise, which starts at exactly
+# 0 and grows to 4-13% of the group maximum within 20 steps (oracle, T_laser).
+# They are compared per array too, but the denominator is floored at a
+# fraction of the group maximum -- 1e-2 of max |E, B| for the fields, 5e-2 of
+# max |J| for the currents:
+# the GPU's J tile accumulates in fixed point with a quantum of 2^-46 of the
+# step's contribution bound, i.e. an absolute J error of
+# ~1e-14 of max |J| (measured on the B200: 2e-14 at step 1 of
+# test_laser_plasma_teacher_forced, where Jy is 7e-4 of max |J|), which a
+# component far below the others cannot meet at 1e-12 of its own maximum;
+# E and B inherit a 1e-15-level error from J through the Yee update.
 SYMMETRY_ZERO = (1, 3, 5, 7)
-FLOOR = 1e-4
+FLOOR_EB, FLOOR_J = 1e-2, 5e-2
 
 
 def open_field_errs(G, F):
@@ -59,7 +66,7 @@ def open_field_errs(G, F):
     for c in range(9):
         den = max(np.abs(F[c]).max(), 1e-300)
         if c in SYMMETRY_ZERO:
-            den = max(den, FLOOR * (se if c < 6 else sj))
+            den = max(den, FLOOR_EB * se if c < 6 else FLOOR_J * sj)
         errs.append(float(np.abs(G[c] - F[c]).max() / den))
     return errs
 
@@ -70,7 +77,7 @@ def _check(sim, orc, wl, tol, what):
     for s in range(len(wl.species)):
         gP, gi = sim.get_particles(s)
         errs += list(compare_state(gP, gi, orc.P[s], orc.ids[s], _L(wl)))
-    assert max(errs) <= tol, (what, errs)
+    assert max(errs) <= tol, (what, [f"{e:.2e}" for e in errs])
     return max(errs)
 
 
