@@ -408,6 +408,15 @@ def run_ours(args, wl, rank, world, local):
     psim.close()
     del psim
     torch.cuda.empty_cache()
+    # per-rank stage split (N > 1): the exchange on its own stream, overlapped
+    # with the interior supercell layers, and the particle stage of every rank
+    by_rank = None
+    if world > 1:
+        import torch.distributed as dist
+        mine = {k: st[k] / args.steps for k in ("sort", "particle", "field", "exchange")}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        by_rank = {k: [g[k] for g in gathered] for k in mine}
     ppc_cells = occupied_cells(wl, slab[0], slab[1])
     n_launch = max(st["particle_launches"], 1)
     per_step_launches = n_launch / args.steps   # species per launch: 1, or all of them (sparse box)
@@ -495,6 +504,7 @@ def run_ours(args, wl, rank, world, local):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "stage_ms_per_step_by_rank": by_rank,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

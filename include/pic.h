@@ -69,6 +69,13 @@ typedef struct pic_config {
     double w[PIC_MAX_SPECIES];         /* weight = real particles per macro-particle */
     int64_t capacity[PIC_MAX_SPECIES]; /* max particles held by this rank, per species */
     int64_t supercell;                 /* S: supercell edge (cells); must divide nx, ny, local nz */
+    int64_t halo;                      /* h: tile drift halo (cells) of the fused particle kernel,
+                                          1 or 2 (0 = 1).  A CTA's shared E/B and J tiles cover
+                                          its supercell plus h cells on every side, so a particle
+                                          may drift h cells out of the supercell it was sorted
+                                          into before it takes the slower global path
+                                          (the supercell's grid data must fit
+                                          on-chip); a larger h allows a larger sort_every */
     int64_t sort_every;                /* K: re-sort at the start of step n when n % K == 0 (0: never) */
     int64_t rank, nranks;              /* z-slab rank / count (1 for a single GPU) */
     int64_t flags;                     /* PIC_FLAG_* bits */

@@ -21,7 +21,14 @@
 
 namespace pic {
 
-constexpr int kGhost = 2;   // G: CIC gather needs [-1, n], VB edges need [-1, n+1]
+// G: the CIC gather needs [-1, n], the VB edges [-1, n+1] (positions are
+// wrapped into the box or slab, so deposits and gathers stay inside [-1, n+1]
+// whatever the tile halo); the TMA box of a fused-kernel tile starts H + 1
+// cells below its supercell and is zero-filled where it leaves the array
+#ifndef PIC_GHOST
+#define PIC_GHOST 2
+#endif
+constexpr int kGhost = PIC_GHOST;
 
 // error bits of the sticky device error word
 enum : unsigned {
@@ -30,6 +37,7 @@ enum : unsigned {
     kErrCapacity = 4u,
     kErrRange = 8u,
     kErrCheck = 16u,   // an internal index check of a PIC_CHECK build failed
+    kErrLateMigration = 32u,   // an interior-layer particle left the slab (overlap bound violated)
 };
 
 // Internal index checks of a debugging build (make CHECK=1 -> -DPIC_CHECK):
@@ -62,6 +70,7 @@ struct GridDev {
     double dt, c;
     double Lx, Ly, Lz;       // global periodic lengths
     int S;                   // supercell edge
+    int H;                   // tile drift halo of the fused kernel (pic_config.halo)
     int nsx, nsy, nsz;       // supercells per axis (local)
     bool periodic_z_local;   // nranks == 1: z ghosts are local images
     int nranks, rank;        // z slabs

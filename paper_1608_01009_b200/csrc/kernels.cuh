@@ -72,8 +72,8 @@ void launch_push_tail(const GridDev &g, const double *EB, double *J, const Parti
                       cudaStream_t st);
 
 // ---- push_tile.cu : fused supercell kernel ----
-bool tile_supported(int S);
-void tile_box(int S, int box[4]);   // TMA box of the E/B tile (x pitch, y, z, comps)
+bool tile_supported(int S, int H);
+void tile_box(int S, int H, int box[4]);   // TMA box of the E/B tile (x pitch, y, z, comps)
 // max |u|^2 of n particles -> *out (high 32 bits of the fp64 value)
 void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t st);
 void configure_tile_kernels();
@@ -86,9 +86,15 @@ struct TileSpecies {
     SpeciesDev sp[kTileMaxSpecies];
     int n;
 };
-// mean_per_sc: particles per supercell over all species (splits very dense supercells)
+// mean_per_sc: particles per supercell over all species (splits very dense supercells).
+// part 0 pushes every supercell layer; with z slabs, part 1 the zb layers at
+// each z end of the slab (the only ones whose particles can deposit into the
+// exchanged J ghost planes or leave the slab this step, runtime.cu
+// boundary_layers) and part 2 the layers in between (a no-op when part 1
+// covered them all).
 void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
-                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st);
+                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb,
+                      cudaStream_t st);
 
 // ---- sort.cu : stable counting sort by (supercell, local cell) ----
 struct SortScratch {
@@ -123,6 +129,9 @@ void launch_j_ghost_add(const GridDev &g, double *J, const double *recv_dn, cons
                         cudaStream_t st);
 // header (count, capped) of a migration send buffer, capacity check
 void launch_mig_finalize(const MigrateDev &m, unsigned *err, cudaStream_t st);
+// after the interior part of an overlapped push: no particle may have been
+// queued for migration after launch_mig_finalize (the boundary-layer bound)
+void launch_mig_late_check(const MigrateDev &m, unsigned *err, cudaStream_t st);
 // appends the particles of two received migration buffers at the tail of P
 void launch_mig_append(const double *recv0, const double *recv1, int cap, const ParticlesDev &P,
                        int64_t *dev_n, int64_t pcap, unsigned *err, cudaStream_t st);

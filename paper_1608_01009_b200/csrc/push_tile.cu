@@ -30,38 +30,50 @@
 
 namespace pic {
 
-constexpr int kTileThreads = 256;
 constexpr int kQueue = 160;     // per-supercell queue of path remainders (crossing particles)
 constexpr int kFQueue = 256;    // per-supercell queue of particles outside the tile (global path)
-constexpr int kCtasPerSm = 2;
 
-// Shared-memory tile geometry.  Row/plane pitches are padded so that the 32
-// lanes of a warp -- 32 consecutive cells of a 4x4x2 block of the supercell
-// under the slot-major particle order -- hit distinct banks: the E/B row pitch
-// is = 4 (mod 8) doubles (12 for S = 4) and the J (u32) pitches are 12 and
-// = 16 (mod 32).  The E/B pitch is the TMA box width (the extra nodes of the
-// box are out-of-bounds zero fill or unused).
+constexpr int up_mod(int v, int m, int r) { return v + (((r - v % m) % m) + m) % m; }   // >= v, = r (mod m)
+
+// Shared-memory tile geometry of supercell edge S and drift halo H.  Row and
+// plane pitches are padded so that the 32 lanes of a warp -- 32 consecutive
+// cells of a 4x4x2 block of the supercell under the slot-major particle
+// order -- spread over the banks: the E/B row pitch is = 4 (mod 8) doubles
+// (12 for S = 4) and the J (u32) pitches are = 4 (mod 8) and = 16 (mod 32).
+// The E/B pitch is the TMA box width (the extra nodes of the box are
+// out-of-bounds zero fill or unused).  Threads per CTA and CTAs per SM follow
+// from the shared memory: two CTAs of 256 threads when the tiles fit twice,
+// else one CTA of 512 (the same 16 warps per SM, 128 registers).
 template <int S, int H>
 struct TileGeom {
     static constexpr int TE = S + 2 * H + 2;   // E/B tile extent (nodes)
     static constexpr int TJ = S + 2 * H + 3;   // J tile extent (nodes)
-    static constexpr int EPX = (S == 4) ? 12 : TE;            // E/B row pitch (doubles) = TMA box dim 0
-    static constexpr int EPY = EPX * TE;                       // E/B plane pitch
-    static constexpr int NE = EPY * TE;                        // E/B component stride
-    static constexpr int JPX = (S == 4) ? 12 : TJ;             // J row pitch (u32)
-    static constexpr int JPY = (S == 4) ? 112 : JPX * TJ;      // J plane pitch
-    static constexpr int NJ = JPY * TJ;                        // J component stride
-    static_assert(EPX >= TE && JPX >= TJ && JPY >= JPX * TJ, "pitches");
+    // the TMA box must start on a 16-byte boundary in x: when the tile origin
+    // -H-1 (+ the kGhost padding) is odd, the box starts one node lower and
+    // the tile is read from eb + XSH
+    static constexpr int XSH = (kGhost - H - 1) & 1;
+    static constexpr int EPX = (S >= 4) ? up_mod(TE + XSH, 8, 4) : (TE + XSH + 1) / 2 * 2;   // row pitch = TMA box dim 0
+    static constexpr int EPY = EPX * TE;                                  // E/B plane pitch
+    static constexpr int NE = EPY * TE;                                   // E/B component stride
+    static constexpr int JPX = (S >= 4) ? up_mod(TJ, 8, 4) : TJ;          // J row pitch (u32)
+    static constexpr int JPY = (S >= 4) ? up_mod(JPX * TJ, 32, 16) : JPX * TJ;   // J plane pitch
+    static constexpr int NJ = JPY * TJ;                                   // J component stride
+    static_assert(EPX >= TE + XSH && JPX >= TJ && JPY >= JPX * TJ, "pitches");
     static_assert((EPX * 8) % 16 == 0, "TMA box row must be a multiple of 16 bytes");
+    static constexpr size_t tiles = 6 * NE * sizeof(double) + 9 * NJ * sizeof(unsigned);
+    static constexpr int CTAS = tiles + 6 * kQueue * sizeof(double) + 12 * 256 * sizeof(double) < 110 * 1024 ? 2 : 1;
+    static constexpr int NT = CTAS == 2 ? 256 : 512;   // threads per CTA
     // shared-memory layout (byte offsets, 128-B aligned where TMA writes)
     static constexpr size_t off_eb = 0;                                        // [6][NE] fp64
     static constexpr size_t off_part = off_eb + 6 * NE * sizeof(double);       // [2][6][threads] fp64
-    static constexpr size_t off_q = off_part + 12 * kTileThreads * sizeof(double);   // [6][kQueue] fp64
+    static constexpr size_t off_q = off_part + 12 * NT * sizeof(double);       // [6][kQueue] fp64
     static constexpr size_t off_jt = off_q + 6 * kQueue * sizeof(double);      // [9][NJ] u32
     static constexpr size_t off_qcell = off_jt + 9 * NJ * sizeof(unsigned);    // [kQueue] u32
     static constexpr size_t off_fq = off_qcell + (kQueue + 1) * sizeof(unsigned);   // [kFQueue + 1] u32
     static constexpr size_t off_misc = (off_fq + (kFQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
-    static constexpr size_t smem_bytes = off_misc + sizeof(uint64_t);          // 1 mbarrier
+    static constexpr size_t smem_bytes = off_misc + 2 * sizeof(uint64_t);      // 1 mbarrier + the TMEM base
+    static constexpr int TMEM_COLS = 32 * (NT / 128);   // 24 used per warp, 4 warps share a lane quadrant
+    static_assert(smem_bytes <= 227 * 1024, "tiles exceed shared memory");
 };
 
 // ---- deterministic fixed-point J tile ----------------------------------
@@ -76,95 +88,183 @@ struct TileGeom {
 // of the order of the atomics.  The flush rebuilds the int64 sum and converts
 // back with the exact factor 2^-F.
 constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52
-constexpr int64_t kMaxTileParticles = 16383;
+constexpr double kFixRange = 140737488355328.0;  // 2^47: |v| of one accumulated value (see fixed_add)
+// tile counters stay exact for < 2^16 contributions per edge of |v| < 2^47
+// (a particle adds to an edge at most 4 times), with a margin for the
+// floor of the accumulated flushes' high words
+constexpr int64_t kMaxTileParticles = 16000;
+#ifndef PIC_TMEM_ACC
+#define PIC_TMEM_ACC 0
+#endif
 
-// rare path: a particle outside its tile (drifted > H cells since the sort)
-template <bool kGeneral>
-__device__ __forceinline__ void push_outside_tile(const GridDev &g, const double *EB, double *J,
-                                                  const SpeciesDev &sp, double &x, double &y,
-                                                  double &z, double &ux, double &uy, double &uz,
-                                                  unsigned *err)
+// The 12 Villasenor-Buneman edge values of one in-cell segment P1 -> P2
+// (local coordinates of the segment's cell), times the flux
+// factors k and the fixed-point scale 2^F (exact: a power of two), in the
+// order Jx (0,0,0) (0,1,0) (0,0,1) (0,1,1), Jy (0,0,0) (1,0,0) (0,0,1)
+// (1,0,1), Jz (0,0,0) (1,0,0) (0,1,0) (1,1,0) of the cell's edges.
+struct EdgeVals {
+    double v[12];
+};
+
+__device__ __forceinline__ EdgeVals seg_values(double p1x, double p1y, double p1z, double p2x, double p2y,
+                                               double p2z, double kxs, double kys, double kzs)
 {
-    push_one_global<kGeneral>(g, EB, J, sp, x, y, z, ux, uy, uz, err);
+    const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
+    const double mx = 0.5 * (p1x + p2x), my = 0.5 * (p1y + p2y), mz = 0.5 * (p1z + p2z);
+    const double fx = kxs * Dx, fy = kys * Dy, fz = kzs * Dz;
+    const double cxx = Dy * Dz * (1.0 / 12.0);
+    const double cyy = Dx * Dz * (1.0 / 12.0);
+    const double czz = Dx * Dy * (1.0 / 12.0);
+    const double nx = 1.0 - mx, ny = 1.0 - my, nz = 1.0 - mz;
+    EdgeVals e;
+    e.v[0] = fx * fma(ny, nz, cxx);
+    e.v[1] = fx * fma(my, nz, -cxx);
+    e.v[2] = fx * fma(ny, mz, -cxx);
+    e.v[3] = fx * fma(my, mz, cxx);
+    e.v[4] = fy * fma(nx, nz, cyy);
+    e.v[5] = fy * fma(mx, nz, -cyy);
+    e.v[6] = fy * fma(nx, mz, -cyy);
+    e.v[7] = fy * fma(mx, mz, cyy);
+    e.v[8] = fz * fma(nx, ny, czz);
+    e.v[9] = fz * fma(mx, ny, -czz);
+    e.v[10] = fz * fma(nx, my, -czz);
+    e.v[11] = fz * fma(mx, my, czz);
+    return e;
+}
+
+// The 4 edge values of component d (0 = Jx, 1 = Jy, 2 = Jz) of seg_values,
+// with the scaled flux factor ks of that axis.
+__device__ __forceinline__ void seg_values_axis(int d, double p1x, double p1y, double p1z, double p2x, double p2y,
+                                                double p2z, double ks, double v[4])
+{
+    const double D[3] = {p2x - p1x, p2y - p1y, p2z - p1z};
+    const double M[3] = {0.5 * (p1x + p2x), 0.5 * (p1y + p2y), 0.5 * (p1z + p2z)};
+    // the two transverse axes, in the order of seg_values' edge list
+    const int a = d == 0 ? 1 : 0, b = d == 2 ? 1 : 2;
+    const double f = ks * D[d];
+    const double c = D[a] * D[b] * (1.0 / 12.0);
+    const double ma = M[a], mb = M[b], na = 1.0 - ma, nb = 1.0 - mb;
+    v[0] = f * fma(na, nb, c);
+    v[1] = f * fma(ma, nb, -c);
+    v[2] = f * fma(na, mb, -c);
+    v[3] = f * fma(ma, mb, c);
+}
+
+// J-tile offsets of the 12 edges of a cell (order of seg_values)
+template <class T>
+__device__ __forceinline__ constexpr int edge_off(int e)
+{
+    constexpr int PX = T::JPX, PY = T::JPY, NJ = T::NJ;
+    constexpr int off[12] = {0,      PX,         PY,          PX + PY,          NJ,              NJ + 1,
+                             NJ + PY, NJ + 1 + PY, 2 * NJ,     2 * NJ + 1,       2 * NJ + PX,     2 * NJ + 1 + PX};
+    return off[e];
+}
+
+// Adds one scaled value w 2^F to the fixed-point tile entry b: v =
+// round(w 2^F) from one fma against 1.5*2^52 (the low word of the result is
+// v mod 2^32, the high word 0x4338 << 16 + (v >> 32) for |v| < 2^51), split
+// into lo16 | mid16 | hi (signed) over three u32 counters.
+template <class T>
+__device__ __forceinline__ void fixed_add(unsigned *b, double vs)
+{
+    constexpr int NJ = T::NJ;
+    const long long bits = __double_as_longlong(vs + kMagic);
+    const unsigned lo = (unsigned)bits;
+    const unsigned hi = (unsigned)(bits >> 32) - (0x43300000u + 0x80000u);
+    atomicAdd(b, lo & 0xffffu);
+    atomicAdd(b + 3 * NJ, lo >> 16);
+    atomicAdd(b + 6 * NJ, hi);
+}
+
+// Adds the exact integer v (|v| < 2^63) to a tile entry: lo16 | mid16 | hi.
+template <class T>
+__device__ __forceinline__ void fixed_add_int(unsigned *b, long long v)
+{
+    constexpr int NJ = T::NJ;
+    const unsigned lo = (unsigned)v;
+    atomicAdd(b, lo & 0xffffu);
+    atomicAdd(b + 3 * NJ, lo >> 16);
+    atomicAdd(b + 6 * NJ, (unsigned)(int)(v >> 32));
+}
+
+// Flushes a thread's accumulator (sums of n biased bit patterns, see the
+// kernel) into the 12 edges of the cell at jbase.
+template <class T>
+__device__ __forceinline__ void tile_add_acc(unsigned *jt, int jbase, const unsigned long long acc[12], unsigned n)
+{
+    const unsigned long long bias = (unsigned long long)n * 0x4338000000000000ull;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) fixed_add_int<T>(jt + jbase + edge_off<T>(k), (long long)(acc[k] - bias));
+}
+
+// the same from an accumulator held as 24 u32 words (lo, hi per value)
+template <class T>
+__device__ __forceinline__ void tile_add_acc_words(unsigned *jt, int jbase, const uint32_t w[24], unsigned n)
+{
+    const unsigned long long bias = (unsigned long long)n * 0x4338000000000000ull;
+#pragma unroll
+    for (int k = 0; k < 12; ++k)
+        fixed_add_int<T>(jt + jbase + edge_off<T>(k),
+                         (long long)((((unsigned long long)w[2 * k + 1] << 32) | w[2 * k]) - bias));
+}
+
+// component d's 4 values of an accumulator held as 8 u32 words
+template <class T>
+__device__ __forceinline__ void tile_add_acc_words4(unsigned *jt, int jbase, int d, const uint32_t w[8], unsigned n)
+{
+    const unsigned long long bias = (unsigned long long)n * 0x4338000000000000ull;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        fixed_add_int<T>(jt + jbase + edge_off<T>(4 * d + k),
+                         (long long)((((unsigned long long)w[2 * k + 1] << 32) | w[2 * k]) - bias));
+}
+
+template <class T>
+__device__ __forceinline__ void tile_add(unsigned *jt, int jbase, const EdgeVals &e)
+{
+#pragma unroll
+    for (int k = 0; k < 12; ++k) fixed_add<T>(jt + jbase + edge_off<T>(k), e.v[k]);
+}
+
+// The fp64 global fallback of one segment (values beyond the fixed-point
+// range, rare): REDG.F64 of the unscaled values into the padded J.
+template <class T>
+__device__ __forceinline__ void global_add(double *J, int64_t gorigin, const GridDev &g, int jbase,
+                                           const EdgeVals &e, double inv_scale)
+{
+    const int rem = jbase % T::JPY, tx = rem % T::JPX, ty = rem / T::JPX, tz = jbase / T::JPY;
+    const int64_t X = g.X, XY = (int64_t)g.X * g.Y, cs = g.cs;
+    double *b = J + gorigin + tx + X * ty + XY * tz;
+    const int64_t off[12] = {0, X, XY, X + XY, cs, cs + 1, cs + XY, cs + 1 + XY,
+                             2 * cs, 2 * cs + 1, 2 * cs + X, 2 * cs + 1 + X};
+#pragma unroll
+    for (int k = 0; k < 12; ++k) atomicAdd(b + off[k], e.v[k] * inv_scale);
 }
 
 // Deposits one in-cell segment P1 -> P2 (local coordinates of the cell whose
-// J-tile index is jbase) with the 12 Villasenor-Buneman edge values of
-// SURVEY.md a5, each added to the fixed-point tile as computed.  A segment
-// whose values could exceed the fixed-point range (a particle that sped up by
-// more than the 2x headroom since the last step) goes to the fp64 global J
-// instead (REDG).
+// J-tile index is jbase) into the fixed-point tile, or -- a segment whose
+// values could exceed the fixed-point range (a particle that sped up by more
+// than the 2x headroom since the last step) -- into the fp64 global J.
 template <class T>
 __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, int64_t gorigin,
                                             const GridDev &g, double p1x, double p1y, double p1z,
                                             double p2x, double p2y, double p2z, double kx,
-                                            double ky, double kz, double scale, bool fits,
+                                            double ky, double kz, double scale, double inv_scale, bool fits,
                                             unsigned *chk = nullptr)
 {
-    constexpr int PX = T::JPX, PY = T::JPY, NJ = T::NJ;
 #ifdef PIC_CHECK   // the cell's 12 edges lie inside the J tile
     if (chk) {
-        const int tz = jbase / PY, ty = (jbase % PY) / PX, tx = (jbase % PY) % PX;
+        const int tz = jbase / T::JPY, ty = (jbase % T::JPY) / T::JPX, tx = (jbase % T::JPY) % T::JPX;
         PIC_DCHECK(jbase >= 0 && tx + 1 < T::TJ && ty + 1 < T::TJ && tz + 1 < T::TJ, chk);
     }
 #else
     (void)chk;
 #endif
-    const double Dx = p2x - p1x, Dy = p2y - p1y, Dz = p2z - p1z;
-    const double mx = 0.5 * (p1x + p2x), my = 0.5 * (p1y + p2y), mz = 0.5 * (p1z + p2z);
-    const double fx = kx * Dx, fy = ky * Dy, fz = kz * Dz;
-    const double cxx = Dy * Dz * (1.0 / 12.0);
-    const double cyy = Dx * Dz * (1.0 / 12.0);
-    const double czz = Dx * Dy * (1.0 / 12.0);
-    const double nx = 1.0 - mx, ny = 1.0 - my, nz = 1.0 - mz;
-    // |value| <= |f| (1 + 1/12): weights are products of numbers in [0,1], |c| <= 1/12.
-    // f scaled by 2^F (exact): one fma per value then rounds f W 2^F + 1.5*2^52.
-    const double fxs = fx * scale, fys = fy * scale, fzs = fz * scale;
-    if (!fits) {   // values beyond the fixed-point range (rare): fp64 global atomics
-        const int rem = jbase % PY, tx = rem % PX, ty = rem / PX, tz = jbase / PY;
-        const int64_t X = g.X, XY = (int64_t)g.X * g.Y, cs = g.cs;
-        double *b = J + gorigin + tx + X * ty + XY * tz;
-        atomicAdd(b, fx * fma(ny, nz, cxx));
-        atomicAdd(b + X, fx * fma(my, nz, -cxx));
-        atomicAdd(b + XY, fx * fma(ny, mz, -cxx));
-        atomicAdd(b + X + XY, fx * fma(my, mz, cxx));
-        atomicAdd(b + cs, fy * fma(nx, nz, cyy));
-        atomicAdd(b + cs + 1, fy * fma(mx, nz, -cyy));
-        atomicAdd(b + cs + XY, fy * fma(nx, mz, -cyy));
-        atomicAdd(b + cs + 1 + XY, fy * fma(mx, mz, cyy));
-        atomicAdd(b + 2 * cs, fz * fma(nx, ny, czz));
-        atomicAdd(b + 2 * cs + 1, fz * fma(mx, ny, -czz));
-        atomicAdd(b + 2 * cs + X, fz * fma(nx, my, -czz));
-        atomicAdd(b + 2 * cs + 1 + X, fz * fma(mx, my, czz));
-        return;
-    }
-    unsigned *b = jt + jbase;
-    // v = round(f W 2^F): the low word of y = v + 1.5*2^52 is v mod 2^32, the
-    // high word is 0x433 << 20 | (2^19 + (v >> 32))
-    auto add = [&](int off, double fs, double w) {
-        const long long bits = __double_as_longlong(fma(fs, w, kMagic));
-        const unsigned lo = (unsigned)bits;
-        const unsigned hi = (unsigned)(bits >> 32) - (0x43300000u + 0x80000u);
-#ifdef PIC_EXP_NOATOMICS   // timing experiment only: drop the tile atomics
-        if (lo == 0x12345u && hi == 0x777u) b[off] = 1u;
-#else
-        atomicAdd(b + off, lo & 0xffffu);
-        atomicAdd(b + 3 * NJ + off, lo >> 16);
-        atomicAdd(b + 6 * NJ + off, hi);
-#endif
-    };
-    add(0, fxs, fma(ny, nz, cxx));
-    add(PX, fxs, fma(my, nz, -cxx));
-    add(PY, fxs, fma(ny, mz, -cxx));
-    add(PX + PY, fxs, fma(my, mz, cxx));
-    add(NJ, fys, fma(nx, nz, cyy));
-    add(NJ + 1, fys, fma(mx, nz, -cyy));
-    add(NJ + PY, fys, fma(nx, mz, -cyy));
-    add(NJ + 1 + PY, fys, fma(mx, mz, cyy));
-    add(2 * NJ, fzs, fma(nx, ny, czz));
-    add(2 * NJ + 1, fzs, fma(mx, ny, -czz));
-    add(2 * NJ + PX, fzs, fma(nx, my, -czz));
-    add(2 * NJ + 1 + PX, fzs, fma(mx, my, czz));
+    const EdgeVals e = seg_values(p1x, p1y, p1z, p2x, p2y, p2z, kx * scale, ky * scale, kz * scale);
+    if (fits)
+        tile_add<T>(jt, jbase, e);
+    else
+        global_add<T>(J, gorigin, g, jbase, e, inv_scale);
 }
 
 // Do the tile values of a particle's path fit the fixed-point range?  Every
@@ -175,7 +275,7 @@ __device__ __forceinline__ void deposit_seg(unsigned *jt, int jbase, double *J, 
 __device__ __forceinline__ bool fits_tile(double dx, double dy, double dz, double kx, double ky, double kz,
                                           double scale)
 {
-    return fmax(fabs(kx * dx), fmax(fabs(ky * dy), fabs(kz * dz))) * scale * (13.0 / 12.0) < 140737488355328.0;
+    return fmax(fabs(kx * dx), fmax(fabs(ky * dy), fabs(kz * dz))) * scale * (13.0 / 12.0) < kFixRange;
 }
 
 // Deposits the rest of a split path (<= 2 more face crossings) starting in
@@ -184,15 +284,15 @@ template <class T>
 __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *J, int64_t gorigin,
                                                   const GridDev &g, double a0, double a1,
                                                   double a2, double b0, double b1, double b2,
-                                                  double kx, double ky, double kz, double scale, bool fits,
-                                                  unsigned *chk = nullptr)
+                                                  double kx, double ky, double kz, double scale,
+                                                  double inv_scale, bool fits, unsigned *chk = nullptr)
 {
 #pragma unroll 1
     for (int it = 0; it < 3; ++it) {
         double e0, e1, e2, r1[3], r2[3];
         int ox, oy, oz;
         const bool more = vb_first_piece(a0, a1, a2, b0, b1, b2, e0, e1, e2, r1, r2, ox, oy, oz);
-        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale, fits, chk);
+        deposit_seg<T>(jt, jb, J, gorigin, g, a0, a1, a2, e0, e1, e2, kx, ky, kz, scale, inv_scale, fits, chk);
         if (!more) break;
         jb += ox + T::JPX * oy + T::JPY * oz;
         a0 = r1[0]; a1 = r1[1]; a2 = r1[2];
@@ -200,8 +300,6 @@ __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *
     }
 }
 
-// kGeneral: slabs (nranks > 1) or an open z box (migration / absorption
-// in the final store); false for the single-domain periodic box.
 // One CTA pushes every species of its supercell in turn, so the E/B tile
 // is loaded and the J tile zeroed and flushed once per supercell and step.
 // kGeneral: slabs (nranks > 1) or an open z box (migration / absorption
@@ -212,16 +310,18 @@ __device__ __forceinline__ void deposit_remainder(unsigned *jt, int jb, double *
 // tile load, the J-tile zeroing and flush and the loop's ragged last
 // iteration are paid once per supercell, and the loop body is not duplicated.
 template <int S, int H, bool kGeneral, int NSP>
-__global__ void __launch_bounds__(kTileThreads, kCtasPerSm)
+__global__ void __launch_bounds__(TileGeom<S, H>::NT, TileGeom<S, H>::CTAS)
 k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double *__restrict__ EB,
-            double *__restrict__ J, const __grid_constant__ TileSpecies ts, int split, unsigned *err)
+            double *__restrict__ J, const __grid_constant__ TileSpecies ts, int split, int zlo_n, int zhi0,
+            unsigned *err)
 {
     static_assert(NSP == 1 || NSP == 2, "one or two species per launch");
     using T = TileGeom<S, H>;
-    constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = kTileThreads;
+    constexpr int TJ = T::TJ, NE = T::NE, NJ = T::NJ, NT = T::NT;
     constexpr int EPX = T::EPX, EPY = T::EPY, JPX = T::JPX, JPY = T::JPY;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *eb = (double *)(smem_raw + T::off_eb);         // [6][TE][TE][EPX]
+    const double *ebx = eb + T::XSH;                       // node (ox, oy, oz) of component 0
     double *pbuf = (double *)(smem_raw + T::off_part);     // [2 stages][6][NT]
     double *q = (double *)(smem_raw + T::off_q);           // [6][kQueue]
     unsigned *jt = (unsigned *)(smem_raw + T::off_jt);     // [3 chunks][3][TJ][JPY/..]
@@ -230,13 +330,16 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     unsigned *fq = (unsigned *)(smem_raw + T::off_fq);     // particles outside the tile
     unsigned *fqcount = fq + kFQueue;
     uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);
-    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t *tmem_slot = (uint32_t *)(smem_raw + T::off_misc + sizeof(uint64_t));
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // `split` CTAs share a supercell, each taking a contiguous part of its
     // particles (short grids fill the last wave; each CTA has its own tiles)
     // grid = (nsx * split, nsy, nsz): no integer divisions on the common path
     const int scx = split == 1 ? (int)blockIdx.x : (int)blockIdx.x / split;
     const int part = split == 1 ? 0 : (int)blockIdx.x % split;
-    const int scy = blockIdx.y, scz = blockIdx.z;
+    // supercell layers of this launch: [0, zlo_n) then [zhi0, ...) (the z-slab
+    // overlap splits a step's push into the boundary layers and the interior)
+    const int scy = blockIdx.y, scz = (int)blockIdx.z < zlo_n ? (int)blockIdx.z : zhi0 + (int)blockIdx.z - zlo_n;
     const int sc = scx + g.nsx * (scy + g.nsy * scz);
     // this CTA's particle range of species s (a part of the supercell's when split)
     auto range = [&](int s, int &a, int &b) {
@@ -253,6 +356,9 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     if (NSP == 2) range(1, a1, b1);
     const int n0 = b0 - a0, total = n0 + (b1 - a1);
     if (total == 0) return;   // empty (uniform per CTA)
+#if PIC_TMEM_ACC
+    if (wid == 0) tmem_alloc(tmem_slot, T::TMEM_COLS);   // read after the __syncthreads below
+#endif
     // concatenated index i -> species (s1: the second one) and its array index p
     auto locate = [&](int i, bool &s1, int &p) {
         s1 = NSP == 2 && i >= n0;
@@ -267,7 +373,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         mbar_init(bar_eb, 1);
         fence_mbar_init();
         mbar_arrive_expect_tx(bar_eb, 6 * NE * sizeof(double));
-        tma_load_4d(eb, &eb_map, ox + kGhost, oy + kGhost, oz + kGhost, 0, bar_eb);
+        tma_load_4d(eb, &eb_map, ox + kGhost - T::XSH, oy + kGhost, oz + kGhost, 0, bar_eb);
     }
     auto stage = [&](int i, int st) {   // this thread's particle i -> its staging slot
         bool s1;
@@ -302,25 +408,78 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         scale = ts.sp[NSP - 1].scale[0];
         inv_scale = ts.sp[NSP - 1].scale[1];
     }
-    double u2loc0 = 0.0, u2loc1 = 0.0;   // this thread's max |u|^2 after the push, per species
+    // this thread's max |u|^2 after the push per species, as the high word of
+    // the fp64 value (non-negative doubles order like their bit patterns)
+    unsigned u2hi0 = 0u, u2hi1 = 0u;
+    // fixed-point range check of a path, folded into the displacement check:
+    // every value of a path is <= |k d| (1 + 1/12) with d its displacement in
+    // cells, so max_a |d_a| < dlim (the smaller of 1 cell and the range bound
+    // over both species and all axes) means "displacement valid and fits the
+    // tile"; a particle past dlim is sorted out exactly on the rare path
+    double kmax = fmax(fabs(ts.sp[0].kx), fmax(fabs(ts.sp[0].ky), fabs(ts.sp[0].kz)));
+    if (NSP == 2)
+        kmax = fmax(kmax, fmax(fabs(ts.sp[NSP - 1].kx), fmax(fabs(ts.sp[NSP - 1].ky), fabs(ts.sp[NSP - 1].kz))));
+    const double dlim = fmin(1.0, kFixRange / (kmax * scale * (13.0 / 12.0)));
     const bool tile_ok = total <= kMaxTileParticles;   // else the counters could overflow
+#if PIC_TMEM_ACC
+    // Per-thread fixed-point accumulator of the first-piece edge values of the
+    // particles whose path starts in the cell acc_cell, kept in TENSOR MEMORY
+    // (TMEM, the per-SM 256 KB array of the 5th-generation tensor cores, here
+    // used as private per-thread storage: warp w owns TMEM lanes 32 (w % 4) ..
+    // and 24 columns at 32 (w / 4), one lane per thread).  It holds the raw
+    // bit patterns of v + 1.5*2^52 summed as u64 (mod 2^64; acc_n of them), so
+    // sum - acc_n * bits(1.5*2^52) is the exact integer sum of the rounded
+    // values and the tile ends up bit-identical to per-particle atomics.  The
+    // slot-major order keeps a thread on one cell of its supercell for as long
+    // as the cells' particle counts allow (always, for a species that does not
+    // move across cells), so those first pieces reach the shared tile -- 36
+    // atomics, each a read and a write wavefront of the shared-memory pipe,
+    // the kernel's binding resource -- once per cell change instead of once
+    // per particle; TMEM traffic does not use that pipe.
+#endif
+    tmem_fence_before_sync();
     __syncthreads();
+    tmem_fence_after_sync();
+#if PIC_TMEM_ACC
+    const uint32_t tmem_base = *tmem_slot;
+    unsigned acc_n = 0u;
+    int acc_cell = -1;
+    // warp w: TMEM lanes 32 (w % 4) .. + 31, columns 32 (w / 4) .. + 23
+    const uint32_t tacc = tmem_base + ((uint32_t)(32 * (wid & 3)) << 16) + 32u * (uint32_t)(wid >> 2);
+    {
+        uint32_t z[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) z[k] = 0u;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) tmem_st8(tacc + 8u * d, z);
+    }
+#endif
     mbar_wait(bar_eb, 0);
 
     int st = 0;
-    for (int i = tid; i < total; i += NT) {
+    // warp-uniform trip count (the TMEM accumulator is updated by the whole
+    // warp every iteration): lanes past the end run the iteration idle
+    for (int i = tid; i - lane < total; i += NT) {
+        const bool valid = i < total;
         if (i + NT < total) stage(i + NT, st ^ 1);   // prefetch the next particle
         cp_async_commit();
         cp_async_wait1();
         bool s1;
         int p;
-        locate(i, s1, p);
+        locate(valid ? i : 0, s1, p);
         const double *pl = pbuf + st * 6 * NT + tid;
         st ^= 1;
-        const double x = pl[0], y = pl[NT], z = pl[2 * NT];
+        const double x = valid ? pl[0] : kDeadX, y = pl[NT], z = pl[2 * NT];
+#if PIC_TMEM_ACC
+        // first piece of this particle's path (start and end in its cell's
+        // coordinates) for the thread's accumulator, added after the branch
+        bool have = false, hs1 = false;
+        int jfirst = 0;
+        double fa0 = 0.0, fa1 = 0.0, fa2 = 0.0, fb0 = 0.0, fb1 = 0.0, fb2 = 0.0;
+#endif
         // dead slot (migrated away or absorbed since the last sort; a single
-        // periodic box has none)
-        if (kGeneral && x < 0.0) continue;
+        // periodic box has none) or a lane past the end
+        if (valid && !(kGeneral && x < 0.0)) {
         double ux = pl[3 * NT], uy = pl[4 * NT], uz = pl[5 * NT];
         const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
         const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
@@ -330,34 +489,18 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                             (unsigned)(ty - 1) < (unsigned)(S + 2 * H) &&
                             (unsigned)(tz - 1) < (unsigned)(S + 2 * H);
         if (inside) {
-#ifdef PIC_EXP_NOGATHER   // timing experiment only: same node for every lane
-            const int hx = 2, hy = 2, hz = 2;
-#define tx 2
-#define ty 2
-#define tz 2
-#else
             const int hx = wx.ih - ox, hy = wy.ih - oy, hz = wz.ih - oz;
-#endif
             // the 8 corners of every component lie inside the E/B tile
             PIC_DCHECK(hx >= 0 && hy >= 0 && hz >= 0 && tx >= 0 && ty >= 0 && tz >= 0 && hx + 1 < T::TE &&
                            hy + 1 < T::TE && hz + 1 < T::TE && tx + 1 < T::TE && ty + 1 < T::TE && tz + 1 < T::TE,
                        err);
-#ifndef PIC_EXP_NOPUSH   // timing experiment only: no gather, no Boris
-            const double ex = trilinear(eb + 0 * NE, hx + EPX * ty + EPY * tz, EPX, EPY, wx.fh, wy.f0, wz.f0);
-            const double ey = trilinear(eb + 1 * NE, tx + EPX * hy + EPY * tz, EPX, EPY, wx.f0, wy.fh, wz.f0);
-            const double ez = trilinear(eb + 2 * NE, tx + EPX * ty + EPY * hz, EPX, EPY, wx.f0, wy.f0, wz.fh);
-            const double bx = trilinear(eb + 3 * NE, tx + EPX * hy + EPY * hz, EPX, EPY, wx.f0, wy.fh, wz.fh);
-            const double by = trilinear(eb + 4 * NE, hx + EPX * ty + EPY * hz, EPX, EPY, wx.fh, wy.f0, wz.fh);
-            const double bz = trilinear(eb + 5 * NE, hx + EPX * hy + EPY * tz, EPX, EPY, wx.fh, wy.fh, wz.f0);
-#ifdef PIC_EXP_NOGATHER
-#undef tx
-#undef ty
-#undef tz
-#endif
+            const double ex = trilinear(ebx + 0 * NE, hx + EPX * ty + EPY * tz, EPX, EPY, wx.fh, wy.f0, wz.f0);
+            const double ey = trilinear(ebx + 1 * NE, tx + EPX * hy + EPY * tz, EPX, EPY, wx.f0, wy.fh, wz.f0);
+            const double ez = trilinear(ebx + 2 * NE, tx + EPX * ty + EPY * hz, EPX, EPY, wx.f0, wy.f0, wz.fh);
+            const double bx = trilinear(ebx + 3 * NE, tx + EPX * hy + EPY * hz, EPX, EPY, wx.f0, wy.fh, wz.fh);
+            const double by = trilinear(ebx + 4 * NE, hx + EPX * ty + EPY * hz, EPX, EPY, wx.fh, wy.f0, wz.fh);
+            const double bz = trilinear(ebx + 5 * NE, hx + EPX * hy + EPY * tz, EPX, EPY, wx.fh, wy.fh, wz.f0);
             boris(s1 ? ts.sp[NSP - 1].h : ts.sp[0].h, ex, ey, ez, bx, by, bz, ux, uy, uz);
-#else
-            (void)hx; (void)hy; (void)hz;
-#endif
             const double u2 = ux * ux + uy * uy + uz * uz;
             const double ig = rsqrt_ge1(1.0 + u2);
             const double xn = fma(cdt * ig, ux, x), yn = fma(cdt * ig, uy, y), zn = fma(cdt * ig, uz, z);
@@ -366,27 +509,47 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             const double byl = yn * g.inv_dy - (double)wy.i0;
             const double bzl = (zn * g.inv_dz - (double)g.k0) - (double)wz.i0;
             const double dxl = bxl - wx.f0, dyl = byl - wy.f0, dzl = bzl - wz.f0;
-            const bool ok = fabs(dxl) < 1.0 && fabs(dyl) < 1.0 && fabs(dzl) < 1.0;
-            if (s1) u2loc1 = fmax(u2loc1, u2); else u2loc0 = fmax(u2loc0, u2);
+            const unsigned h2 = (unsigned)__double2hiint(u2);
+            u2hi0 = max(u2hi0, s1 ? 0u : h2);
+            if (NSP == 2) u2hi1 = max(u2hi1, s1 ? h2 : 0u);
             const ParticlesDev &in = s1 ? ts.in[NSP - 1] : ts.in[0];
             const ParticlesDev &out = s1 ? ts.out[NSP - 1] : ts.out[0];
             const SpeciesDev &sp = s1 ? ts.sp[NSP - 1] : ts.sp[0];
+            const bool fast = fabs(dxl) < dlim && fabs(dyl) < dlim && fabs(dzl) < dlim;
+            bool ok = fast, fits = fast;
+            if (!fast) {   // rare: exactly which of the two failed
+                ok = fabs(dxl) < 1.0 && fabs(dyl) < 1.0 && fabs(dzl) < 1.0;
+                fits = fits_tile(dxl, dyl, dzl, sp.kx, sp.ky, sp.kz, scale);
+            }
             if (ok)
                 store_particle<kGeneral>(g, sp, out, in.id, p, wrap_coord(xn, g.Lx), wrap_coord(yn, g.Ly),
                                          kGeneral ? wrap_z(g, zn) : wrap_coord(zn, g.Lz), ux, uy, uz, false, err);
             else
                 store_particle<kGeneral>(g, sp, out, in.id, p, x, y, z, ux, uy, uz, false, err);
             if (ok) {
-#ifndef PIC_EXP_NODEP   // timing experiment only: no deposit
                 const double kx = sp.kx, ky = sp.ky, kz = sp.kz;   // q w / (dt dA), host
                 const int jbase = tx + JPX * ty + JPY * tz;
                 double ex_, ey_, ez_, r1[3], r2[3];
                 int cx, cy, cz;
                 const bool more =
                     vb_first_piece(wx.f0, wy.f0, wz.f0, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
-                const bool fits = fits_tile(dxl, dyl, dzl, kx, ky, kz, scale);
+#if PIC_TMEM_ACC
+                PIC_DCHECK(jbase >= 0 && tx + 1 < T::TJ && ty + 1 < T::TJ && tz + 1 < T::TJ, err);
+                if (fits) {   // to the TMEM accumulator after the branch (warp-converged)
+                    have = true;
+                    hs1 = s1;
+                    jfirst = jbase;
+                    fa0 = wx.f0; fa1 = wy.f0; fa2 = wz.f0;
+                    fb0 = ex_; fb1 = ey_; fb2 = ez_;
+                } else {
+                    global_add<T>(J, gorigin, g, jbase,
+                                  seg_values(wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx * scale, ky * scale, kz * scale),
+                                  inv_scale);
+                }
+#else
                 deposit_seg<T>(jt, jbase, J, gorigin, g, wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx, ky, kz, scale,
-                               fits, err);
+                               inv_scale, fits, err);
+#endif
                 if (more) {
                     // the rest of a face-crossing path is deposited after the particle
                     // loop, all queued paths together (keeps the loop convergent); the
@@ -405,16 +568,19 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                         qb = __shfl_sync(act, qb, leader);
                         if (fits) slot = qb + (unsigned)__popc(want & ((1u << lane) - 1u));
                     }
+                    // the remainder in the next cell's coordinates: r1 = e - o,
+                    // r2 = b - o (the same subtractions vb_first_piece makes)
+                    const double r10 = ex_ - (double)cx, r11 = ey_ - (double)cy, r12 = ez_ - (double)cz;
+                    const double r20 = bxl - (double)cx, r21 = byl - (double)cy, r22 = bzl - (double)cz;
                     if (slot < (unsigned)kQueue) {
-                        q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
-                        q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
+                        q[0 * kQueue + slot] = r10; q[1 * kQueue + slot] = r11; q[2 * kQueue + slot] = r12;
+                        q[3 * kQueue + slot] = r20; q[4 * kQueue + slot] = r21; q[5 * kQueue + slot] = r22;
                         qcell[slot] = (unsigned)jrem | (s1 ? 0x80000000u : 0u);
                     } else {
-                        deposit_remainder<T>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0], r2[1],
-                                             r2[2], kx, ky, kz, scale, fits, err);
+                        deposit_remainder<T>(jt, jrem, J, gorigin, g, r10, r11, r12, r20, r21, r22, kx, ky, kz,
+                                             scale, inv_scale, fits, err);
                     }
                 }
-#endif
             } else {
                 atomicOr(err, (isfinite(xn) && isfinite(yn) && isfinite(zn)) ? kErrDisplacement
                                                                               : kErrNonFinite);
@@ -430,13 +596,62 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                 const ParticlesDev &out = s1 ? ts.out[NSP - 1] : ts.out[0];
                 const SpeciesDev &sp = s1 ? ts.sp[NSP - 1] : ts.sp[0];
                 double xx = x, yy = y, zz = z;
-                push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+                push_one_global<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
                 store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
-                const double v2 = ux * ux + uy * uy + uz * uz;
-                if (s1) u2loc1 = fmax(u2loc1, v2); else u2loc0 = fmax(u2loc0, v2);
+                const unsigned h2 = (unsigned)__double2hiint(ux * ux + uy * uy + uz * uz);
+                u2hi0 = max(u2hi0, s1 ? 0u : h2);
+                if (NSP == 2) u2hi1 = max(u2hi1, s1 ? h2 : 0u);
             }
         }
+        }   // live slot
+#if PIC_TMEM_ACC
+        // the whole warp, converged: accumulator += this particle's first piece
+        // (a cell change first flushes the old sums to the shared tile); in
+        // three passes of 8 TMEM columns (the 4 edges of Jx, Jy, Jz), which
+        // keeps the registers in flight low
+        __syncwarp();
+        {
+            const SpeciesDev &hsp = hs1 ? ts.sp[NSP - 1] : ts.sp[0];
+            const bool flush = have && jfirst != acc_cell && acc_n;
+            const bool reset = have && jfirst != acc_cell;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                uint32_t r[8];
+                tmem_ld8(tacc + 8u * d, r);
+                if (flush) tile_add_acc_words4<T>(jt, acc_cell, d, r, acc_n);
+                if (have) {
+                    double v4[4];
+                    seg_values_axis(d, fa0, fa1, fa2, fb0, fb1, fb2,
+                                    (d == 0 ? hsp.kx : d == 1 ? hsp.ky : hsp.kz) * scale, v4);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const unsigned long long old =
+                            reset ? 0ull : (((unsigned long long)r[2 * k + 1] << 32) | r[2 * k]);
+                        const unsigned long long v = old + (unsigned long long)__double_as_longlong(v4[k] + kMagic);
+                        r[2 * k] = (uint32_t)v;
+                        r[2 * k + 1] = (uint32_t)(v >> 32);
+                    }
+                }
+                __syncwarp();
+                tmem_st8(tacc + 8u * d, r);
+            }
+            if (reset) {
+                acc_cell = jfirst;
+                acc_n = 0u;
+            }
+            acc_n += have ? 1u : 0u;
+        }
+#endif
     }
+#if PIC_TMEM_ACC
+    __syncwarp();
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        uint32_t r[8];
+        tmem_ld8(tacc + 8u * d, r);
+        if (acc_n) tile_add_acc_words4<T>(jt, acc_cell, d, r, acc_n);
+    }
+#endif
     __syncthreads();   // all particles pushed, the queues are complete
     const int nq = min(*qcount, (unsigned)kQueue);
     for (int e = tid; e < nq; e += NT) {
@@ -444,7 +659,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         const SpeciesDev &sp = (qc >> 31) ? ts.sp[NSP - 1] : ts.sp[0];
         deposit_remainder<T>(jt, (int)(qc & 0x7fffffffu), J, gorigin, g, q[e], q[kQueue + e], q[2 * kQueue + e],
                              q[3 * kQueue + e], q[4 * kQueue + e], q[5 * kQueue + e], sp.kx, sp.ky, sp.kz, scale,
-                             true, err);
+                             inv_scale, true, err);
     }
     const int nf = min(*fqcount, (unsigned)kFQueue);
     for (int e = tid; e < nf; e += NT) {
@@ -455,16 +670,17 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         const ParticlesDev &out = s1 ? ts.out[NSP - 1] : ts.out[0];
         const SpeciesDev &sp = s1 ? ts.sp[NSP - 1] : ts.sp[0];
         double xx = in.x[p], yy = in.y[p], zz = in.z[p], ux = in.ux[p], uy = in.uy[p], uz = in.uz[p];
-        push_outside_tile<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
+        push_one_global<kGeneral>(g, EB, J, sp, xx, yy, zz, ux, uy, uz, err);
         store_particle<kGeneral>(g, sp, out, in.id, p, xx, yy, zz, ux, uy, uz, false, err);
-        const double v2 = ux * ux + uy * uy + uz * uz;
-        if (s1) u2loc1 = fmax(u2loc1, v2); else u2loc0 = fmax(u2loc0, v2);
+        const unsigned h2 = (unsigned)__double2hiint(ux * ux + uy * uy + uz * uz);
+        u2hi0 = max(u2hi0, s1 ? 0u : h2);
+        if (NSP == 2) u2hi1 = max(u2hi1, s1 ? h2 : 0u);
     }
     {
-        const unsigned hi0 = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc0) >> 32));
+        const unsigned hi0 = __reduce_max_sync(0xffffffffu, u2hi0);
         if (lane == 0 && hi0) atomicMax(ts.sp[0].u2max_out, hi0);
         if (NSP == 2) {
-            const unsigned hi1 = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(u2loc1) >> 32));
+            const unsigned hi1 = __reduce_max_sync(0xffffffffu, u2hi1);
             if (lane == 0 && hi1) atomicMax(ts.sp[NSP - 1].u2max_out, hi1);
         }
     }
@@ -474,7 +690,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     // reads hit consecutive banks and the REDGs of a row are coalesced.
     const int64_t cs = g.cs, gsy = g.X, gsz = (int64_t)g.X * g.Y;
     constexpr int kRowsPerWarp = 32 / TJ;
-    const int wid = tid >> 5, a = lane % TJ, rsub = lane / TJ;
+    const int a = lane % TJ, rsub = lane / TJ;
     // a warp takes whole (component, z) planes of the tile, kRowsPerWarp rows
     // at a time, with the plane's base addresses computed once
     if (rsub < kRowsPerWarp) {
@@ -492,6 +708,12 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             }
         }
     }
+#if PIC_TMEM_ACC
+    tmem_fence_before_sync();
+    __syncthreads();   // every warp's TMEM traffic is done
+    tmem_fence_after_sync();
+    if (wid == 0) tmem_dealloc(tmem_base, T::TMEM_COLS);
+#endif
 }
 
 __global__ void __launch_bounds__(256) k_u2max(ParticlesDev P, int64_t n, unsigned *out)
@@ -525,7 +747,7 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 
 template <int S, int H, bool kGeneral>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
-                        const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st)
+                        const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb, cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
     // one CTA per supercell (empty ones exit at once); only very dense
@@ -536,53 +758,82 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
 #define PIC_SPLIT_AT 8192
 #endif
     const int split = (int)std::max<int64_t>(1, std::min<int64_t>(16, (mean_per_sc + PIC_SPLIT_AT - 1) / PIC_SPLIT_AT));
-    const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)g.nsz);
+    // part 0: every supercell layer; 1: the zb layers at each z end of the
+    // slab; 2: the layers in between (see launch_push_tile)
+    int zlo_n = g.nsz, zhi0 = 0, nz_l = g.nsz;
+    if (part != 0 && 2 * zb < g.nsz) {
+        if (part == 1) { zlo_n = zb; zhi0 = g.nsz - zb; nz_l = 2 * zb; }
+        else { zlo_n = 0; zhi0 = zb; nz_l = g.nsz - 2 * zb; }
+    } else if (part == 2) {
+        return;   // the boundary part covered every layer
+    }
+    const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)nz_l);
     if (ts.n == 1)
-        k_push_tile<S, H, kGeneral, 1><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err);
+        k_push_tile<S, H, kGeneral, 1><<<grid, TileGeom<S, H>::NT, smem, st>>>(map, g, EB, J, ts, split, zlo_n, zhi0, err);
     else
-        k_push_tile<S, H, kGeneral, 2><<<grid, kTileThreads, smem, st>>>(map, g, EB, J, ts, split, err);
+        k_push_tile<S, H, kGeneral, 2><<<grid, TileGeom<S, H>::NT, smem, st>>>(map, g, EB, J, ts, split, zlo_n, zhi0, err);
 }
 
-bool tile_supported(int S) { return S == 2 || S == 4; }
+bool tile_supported(int S, int H) { return (S == 2 || S == 4) && (H == 1 || H == 2); }
 
-void tile_box(int S, int box[4])
+template <int S, int H>
+static void box_of(int box[4])
 {
-    const int te = S + 2 * 1 + 2;
-    box[0] = (S == 4) ? TileGeom<4, 1>::EPX : TileGeom<2, 1>::EPX;
-    box[1] = te;
-    box[2] = te;
+    box[0] = TileGeom<S, H>::EPX;
+    box[1] = TileGeom<S, H>::TE;
+    box[2] = TileGeom<S, H>::TE;
     box[3] = 6;
 }
 
-template <int S, bool G>
+void tile_box(int S, int H, int box[4])
+{
+    if (S == 4 && H == 1) box_of<4, 1>(box);
+    else if (S == 4 && H == 2) box_of<4, 2>(box);
+    else if (S == 2 && H == 1) box_of<2, 1>(box);
+    else box_of<2, 2>(box);
+}
+
+template <int S, int H, bool G>
 static void set_smem()
 {
-    const int b = (int)TileGeom<S, 1>::smem_bytes;
-    cudaFuncSetAttribute(k_push_tile<S, 1, G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute(k_push_tile<S, 1, G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    const int b = (int)TileGeom<S, H>::smem_bytes;
+    cudaFuncSetAttribute(k_push_tile<S, H, G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute(k_push_tile<S, H, G, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
+template <int S, int H>
+static void set_smem_both()
+{
+    set_smem<S, H, false>();
+    set_smem<S, H, true>();
 }
 
 void configure_tile_kernels()
 {
-    set_smem<4, false>();
-    set_smem<4, true>();
-    set_smem<2, false>();
-    set_smem<2, true>();
+    set_smem_both<4, 1>();
+    set_smem_both<4, 2>();
+    set_smem_both<2, 1>();
+    set_smem_both<2, 2>();
+}
+
+template <int S, int H>
+static void launch_sh(const CUtensorMap &map, const GridDev &g, const double *EB, double *J, const TileSpecies &ts,
+                      unsigned *err, int64_t mean_per_sc, int part, int zb, cudaStream_t st)
+{
+    if (g.nranks > 1 || g.open_z)
+        launch_tile<S, H, true>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+    else
+        launch_tile<S, H, false>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
 }
 
 void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
-                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, cudaStream_t st)
+                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb, cudaStream_t st)
 {
     if (ts.n == 0) return;
-    const bool general = g.nranks > 1 || g.open_z;
-    if (g.S == 4 && general)
-        launch_tile<4, 1, true>(map, g, EB, J, ts, err, mean_per_sc, st);
-    else if (g.S == 4)
-        launch_tile<4, 1, false>(map, g, EB, J, ts, err, mean_per_sc, st);
-    else if (g.S == 2 && general)
-        launch_tile<2, 1, true>(map, g, EB, J, ts, err, mean_per_sc, st);
-    else if (g.S == 2)
-        launch_tile<2, 1, false>(map, g, EB, J, ts, err, mean_per_sc, st);
+    if (g.S == 4 && g.H == 1) launch_sh<4, 1>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+    else if (g.S == 4 && g.H == 2) launch_sh<4, 2>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+    else if (g.S == 2 && g.H == 1) launch_sh<2, 1>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+    else if (g.S == 2 && g.H == 2) launch_sh<2, 2>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
 }
 
 }  // namespace pic

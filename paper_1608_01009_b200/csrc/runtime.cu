@@ -76,6 +76,7 @@ std::string validate(const pic_config *c)
     }
     if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return "bad rank / nranks";
     if (c->supercell < 1) return "supercell must be >= 1";
+    if (c->halo < 0 || c->halo > 2) return "halo must be 1 or 2 (0 = 1)";
     if (c->bc_z != PIC_BC_PERIODIC && c->bc_z != PIC_BC_OPEN) return "bc_z must be PIC_BC_PERIODIC or PIC_BC_OPEN";
     if (c->bc_z == PIC_BC_OPEN && c->nz < 3) return "an open z box needs nz >= 3";
     if (c->bc_z == PIC_BC_OPEN &&
@@ -112,7 +113,7 @@ Layout make_layout(const pic_config *c)
     g.nz_global = (int)c->nz;
     g.k0 = (int)(explicit_slab ? c->slab_lo : c->rank * g.nz);
     g.X = g.nx + 2 * kGhost;
-    g.X += g.X & 1;   // 16-byte row pitch (TMA global strides)
+    g.X = (g.X + 3) / 4 * 4;   // 32-byte rows (TMA global strides need 16; tile boxes start 32-byte aligned)
     g.Y = g.ny + 2 * kGhost;
     g.Z = g.nz + 2 * kGhost;
     g.cs = (int64_t)g.X * g.Y * g.Z;
@@ -122,6 +123,7 @@ Layout make_layout(const pic_config *c)
     g.dt = c->dt; g.c = c->c;
     g.Lx = c->nx * c->dx; g.Ly = c->ny * c->dy; g.Lz = c->nz * c->dz;
     g.S = (int)c->supercell;
+    g.H = c->halo ? (int)c->halo : 1;
     g.nsx = g.nx / g.S; g.nsy = g.ny / g.S; g.nsz = g.nz / g.S;
     g.open_z = c->bc_z == PIC_BC_OPEN;
     g.periodic_z_local = (c->nranks == 1) && !g.open_z;
@@ -313,6 +315,12 @@ struct pic_ctx {
     CUtensorMap eb_map;        // TMA descriptor of the padded E/B array [6][Z][Y][X]
     int num_sms = 148;
     ncclComm_t comm = nullptr;
+    // z slabs: the J ghost / migration exchange of a step runs on st_x while
+    // the interior supercell layers are pushed on st (fork/join by events,
+    // captured in the step graph); zb = boundary layers per slab end
+    cudaStream_t st_x = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int zb = 0;
     std::string last_error;
     // graphs keyed by (sort_now, jcur)
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -439,8 +447,9 @@ bool has_neighbour(const pic_config &c, int rank, int dir)
     return dir == 0 ? rank > 0 : rank < c.nranks - 1;
 }
 
-int exchange_nccl(pic_ctx *ctx, const std::vector<Msg> &msgs)
+int exchange_nccl(pic_ctx *ctx, const std::vector<Msg> &msgs, cudaStream_t st = nullptr)
 {
+    if (!st) st = ctx->st;
     NcclApi *api = nccl_api();
     if (!api || !ctx->comm) return fail(ctx, PIC_ENCCL, "NCCL not initialised");
     const int r = (int)ctx->cfg.rank, n = (int)ctx->cfg.nranks;
@@ -452,10 +461,10 @@ int exchange_nccl(pic_ctx *ctx, const std::vector<Msg> &msgs)
     // direction d goes to the neighbour on side d and arrives from the other side
     for (const Msg &m : msgs)
         if (e == ncclSuccess && (m.dir == 0 ? has_dn : has_up))
-            e = api->send(m.send, m.count, ncclFloat64, m.dir == 0 ? dn : up, ctx->comm, ctx->st);
+            e = api->send(m.send, m.count, ncclFloat64, m.dir == 0 ? dn : up, ctx->comm, st);
     for (const Msg &m : msgs)
         if (e == ncclSuccess && (m.dir == 0 ? has_up : has_dn))
-            e = api->recv(m.recv, m.count, ncclFloat64, m.dir == 0 ? up : dn, ctx->comm, ctx->st);
+            e = api->recv(m.recv, m.count, ncclFloat64, m.dir == 0 ? up : dn, ctx->comm, st);
     const ncclResult_t e2 = api->groupEnd();
     if (e != ncclSuccess || e2 != ncclSuccess)
         return fail(ctx, PIC_ENCCL, std::string("NCCL exchange: ") +
@@ -479,12 +488,16 @@ int exchange_local(pic_ctx *const *ctxs, int n, const std::vector<std::vector<Ms
 }
 
 // ---- the phases of one step; each returns the number of kernel launches ----
-int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
+// part 0: the whole push; with z slabs part 1 = sort + the boundary supercell
+// layers + the tail kernel + migration headers (everything the step's first
+// exchange needs), part 2 = the interior layers (run while that exchange is
+// in flight) + the check that none of them migrated
+int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile, int part = 0)
 {
     const Layout &L = ctx->L;
     const GridDev &g = L.g;
     int launches = 0;
-    if (sort_now) {
+    if (sort_now && part != 2) {
         StageMark m(ctx, 0, profile);
         for (int s = 0; s < ctx->cfg.n_species; ++s)
             if (ctx->has_particles[s]) {
@@ -516,7 +529,7 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
             ++ts.n;
             if (ts.n == 2) {   // a launch takes one or two species
                 launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], ts, ctx->err,
-                                 cap_total / std::max<int64_t>(1, L.n_sc), ctx->st);
+                                 cap_total / std::max<int64_t>(1, L.n_sc), part, ctx->zb, ctx->st);
                 ++launches;
                 if (profile) ctx->particle_launches++;
                 ts.n = 0;
@@ -525,7 +538,7 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
         }
         if (ts.n > 0) {
             launch_push_tile(ctx->eb_map, g, ctx->EB, ctx->J[jcur], ts, ctx->err,
-                             cap_total / std::max<int64_t>(1, L.n_sc), ctx->st);
+                             cap_total / std::max<int64_t>(1, L.n_sc), part, ctx->zb, ctx->st);
             ++launches;
             if (profile) ctx->particle_launches++;
         }
@@ -533,14 +546,14 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
     for (int s = 0; s < ctx->cfg.n_species; ++s) {
         if (!ctx->has_particles[s]) continue;
         const SpeciesDev sp = species_dev(ctx, s, jcur);
-        if (!ctx->use_tile) {
+        if (!ctx->use_tile && part != 2) {
             const ParticlesDev &in = sort_now ? ctx->B[s] : ctx->A[s];
             launch_push_tail(g, ctx->EB, ctx->J[jcur], in, ctx->A[s], nullptr, ctx->dev_n + s, L.cap[s], sp,
                              sort_now, ctx->err, ctx->st);
             ++launches;
             if (profile) ctx->particle_launches++;
         }
-        if (ctx->slabs) {
+        if (ctx->slabs && part != 2) {
             if (ctx->use_tile) {   // particles received since the last sort (none right after it)
                 if (!sort_now) {
                     launch_push_tail(g, ctx->EB, ctx->J[jcur], ctx->A[s], ctx->A[s], ctx->sc_off[s] + L.n_sc,
@@ -551,8 +564,27 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
             launch_mig_finalize(ctx->mig[s], ctx->err, ctx->st);
             ++launches;
         }
+        if (ctx->slabs && part == 2 && ctx->use_tile) {
+            launch_mig_late_check(ctx->mig[s], ctx->err, ctx->st);
+            ++launches;
+        }
     }
     return launches;
+}
+
+// Supercell layers per slab end whose particles may, this step, deposit into
+// the exchanged J ghost planes or leave the slab: a particle moves less than
+// c dt per step on each axis, so one sorted into layer l >= zb (z >= zb S dz
+// above the slab's lower face) is still at z >= dz after the <= K - 1 steps
+// since the sort, and its path of this step stays inside [0, nz) -- no
+// deposit below plane 0, no migration; likewise at the upper face.  Without
+// periodic re-sorts (K = 0) every layer is a boundary layer.
+int boundary_layers(const pic_config &c, const GridDev &g)
+{
+    if (c.sort_every <= 0) return g.nsz;
+    const double drift = (double)(c.sort_every - 1) * c.c * c.dt / c.dz;   // cells
+    const int zb = (int)std::ceil((1.0 + drift) / g.S + 1e-12);
+    return std::min(zb, g.nsz);
 }
 
 // J-tile scale preparation from the u^2 bound of parity `from` (the step that
@@ -629,10 +661,32 @@ void refresh_bh(pic_ctx *ctx)
 // a whole step on one rank (NCCL exchanges or none); returns launches or < 0
 int enqueue_step(pic_ctx *ctx, bool sort_now, int jcur, bool profile)
 {
-    int launches = phase_push(ctx, sort_now, jcur, profile);
+    int launches = 0;
     if (ctx->slabs) {
-        StageMark m(ctx, 3, profile);
-        if (exchange_nccl(ctx, msgs_current(ctx, jcur)) != PIC_OK) return -1;
+        // boundary layers first; their J ghost planes and the migrating
+        // particles go out on st_x while the interior layers are pushed on st
+        launches += phase_push(ctx, sort_now, jcur, profile, 1);
+        if (cudaEventRecord(ctx->ev_fork, ctx->st) != cudaSuccess ||
+            cudaStreamWaitEvent(ctx->st_x, ctx->ev_fork, 0) != cudaSuccess)
+            return -1;
+        {
+            cudaEvent_t a = nullptr;
+            if (profile) {
+                a = take_event(ctx);
+                cudaEventRecord(a, ctx->st_x);
+            }
+            if (exchange_nccl(ctx, msgs_current(ctx, jcur), ctx->st_x) != PIC_OK) return -1;
+            if (profile) {
+                cudaEvent_t b = take_event(ctx);
+                cudaEventRecord(b, ctx->st_x);
+                ctx->ev_marks.push_back({3, {a, b}});
+            }
+        }
+        if (cudaEventRecord(ctx->ev_join, ctx->st_x) != cudaSuccess) return -1;
+        launches += phase_push(ctx, sort_now, jcur, profile, 2);
+        if (cudaStreamWaitEvent(ctx->st, ctx->ev_join, 0) != cudaSuccess) return -1;
+    } else {
+        launches += phase_push(ctx, sort_now, jcur, profile);
     }
     launches += phase_fields_e(ctx, jcur, profile);
     if (ctx->slabs) {
@@ -691,7 +745,7 @@ int encode_eb_map(pic_ctx *ctx)
     auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
     const GridDev &g = ctx->L.g;
     int bx[4];
-    tile_box(g.S, bx);
+    tile_box(g.S, g.H, bx);
     cuuint64_t dims[4] = {(cuuint64_t)g.X, (cuuint64_t)g.Y, (cuuint64_t)g.Z, 6};
     cuuint64_t strides[3] = {sizeof(double) * (cuuint64_t)g.X, sizeof(double) * (cuuint64_t)g.X * g.Y,
                              sizeof(double) * (cuuint64_t)g.cs};
@@ -714,6 +768,8 @@ int check_device_error(pic_ctx *ctx)
     if (h & kErrRange) return fail(ctx, PIC_EINVAL, "particle position outside the domain / slab");
     if (h & kErrCapacity) return fail(ctx, PIC_ECAPACITY, "device capacity exceeded (particles or migration)");
     if (h & kErrCheck) return fail(ctx, PIC_ECUDA, "internal index check failed (PIC_CHECK build)");
+    if (h & kErrLateMigration)
+        return fail(ctx, PIC_ECUDA, "an interior supercell layer's particle left the slab (overlap bound violated)");
     return PIC_OK;
 }
 
@@ -879,7 +935,7 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
     ctx->laser_par[3] = cfg->laser_t0;
     ctx->laser_par[4] = cfg->laser_pol[0];
     ctx->laser_par[5] = cfg->laser_pol[1];
-    ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell);
+    ctx->use_tile = !(cfg->flags & PIC_FLAG_NAIVE) && tile_supported((int)cfg->supercell, ctx->L.g.H);
     configure_tile_kernels();
     {
         int dev = 0;
@@ -907,12 +963,22 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
         delete ctx;
         return PIC_ECUDA;
     }
+    if (ctx->slabs) {
+        ctx->zb = boundary_layers(*cfg, L.g);
+        if (!ctx->local_group &&
+            (cudaStreamCreateWithFlags(&ctx->st_x, cudaStreamNonBlocking) != cudaSuccess ||
+             cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+             cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+            pic_destroy(ctx);
+            return PIC_ECUDA;
+        }
+    }
     if (ctx->slabs && !ctx->local_group) {
         NcclApi *api = nccl_api();
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_id, 128);
         if (!api || api->commInitRank(&ctx->comm, (int)cfg->nranks, id, (int)cfg->rank) != ncclSuccess) {
-            delete ctx;
+            pic_destroy(ctx);
             return PIC_ENCCL;
         }
     }
@@ -1173,9 +1239,12 @@ int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps)
         const int64_t K = ctxs[0]->cfg.sort_every;
         const bool sort_now = K > 0 && (ctxs[0]->step_index % K) == 0;
         const int jc = ctxs[0]->jcur;
-        for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_push(ctxs[r], sort_now, jc, false);
+        // the same boundary / exchange / interior order as a NCCL step (the
+        // copies here are ordered on each context's stream)
+        for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_push(ctxs[r], sort_now, jc, false, 1);
         int rc = exchange_local(ctxs, n, all([jc](pic_ctx *c) { return msgs_current(c, jc); }));
         if (rc != PIC_OK) return rc;
+        for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_push(ctxs[r], sort_now, jc, false, 2);
         for (int r = 0; r < n; ++r) ctxs[r]->launches += phase_fields_e(ctxs[r], jc, false);
         rc = exchange_local(ctxs, n, all([](pic_ctx *c) { return msgs_fields(c, 0, 3); }));
         if (rc != PIC_OK) return rc;
@@ -1345,6 +1414,9 @@ void pic_destroy(pic_ctx *ctx)
         NcclApi *api = nccl_api();
         if (api) api->commDestroy(ctx->comm);
     }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->st_x) cudaStreamDestroy(ctx->st_x);
     delete ctx;
 }
 

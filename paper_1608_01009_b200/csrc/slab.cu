@@ -25,7 +25,7 @@ k_j_ghost_add(GridDev g, double *__restrict__ J, const double *__restrict__ rdn,
     const int64_t r = t - comp * per_comp;          // [2 planes][Y][X]
     double *Jc = J + comp * g.cs;
     // padded plane index of local plane k is k + kGhost
-    const int64_t lo_ghost = 0 * plane + r;                        // planes -2, -1
+    const int64_t lo_ghost = (int64_t)(kGhost - 2) * plane + r;    // planes -2, -1
     const int64_t hi_ghost = (int64_t)(g.nz + kGhost) * plane + r; // planes nz, nz+1
     const int64_t lo_int = (int64_t)kGhost * plane + r;            // planes 0, 1
     const int64_t hi_int = (int64_t)g.nz * plane + r;              // planes nz-2, nz-1
@@ -57,6 +57,16 @@ __global__ void k_mig_finalize(MigrateDev m, unsigned *err)
 void launch_mig_finalize(const MigrateDev &m, unsigned *err, cudaStream_t st)
 {
     k_mig_finalize<<<1, 32, 0, st>>>(m, err);
+}
+
+__global__ void k_mig_late_check(MigrateDev m, unsigned *err)
+{
+    if (threadIdx.x < 2 && m.count[threadIdx.x] != 0u) atomicOr(err, kErrLateMigration);
+}
+
+void launch_mig_late_check(const MigrateDev &m, unsigned *err, cudaStream_t st)
+{
+    k_mig_late_check<<<1, 32, 0, st>>>(m, err);
 }
 
 // appends received particles (two buffers) at [*dev_n, *dev_n + c0 + c1)

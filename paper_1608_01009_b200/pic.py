@@ -47,6 +47,7 @@ class PicConfig(C.Structure):
         ("w", C.c_double * MAX_SPECIES),
         ("capacity", C.c_int64 * MAX_SPECIES),
         ("supercell", C.c_int64),
+        ("halo", C.c_int64),
         ("sort_every", C.c_int64),
         ("rank", C.c_int64), ("nranks", C.c_int64),
         ("flags", C.c_int64),
@@ -159,7 +160,7 @@ def _dptr(a):
 
 def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity=None,
                 supercell=4, sort_every=20, rank=0, nranks=1, flags=0, nccl_id=None,
-                migrate_capacity=0, bc_z=BC_PERIODIC, slab=None, laser=None):
+                migrate_capacity=0, bc_z=BC_PERIODIC, slab=None, laser=None, halo=1):
     """species: list of (q, m, w); slab: (lo, hi) planes of this rank;
     laser: dict e0, omega, ramp, t0, pol (open z, NEXT-1)."""
     cfg = PicConfig()
@@ -170,7 +171,7 @@ def make_config(nx, ny, nz, species, dt, dx=1.0, dy=1.0, dz=1.0, c=1.0, capacity
     for i, (q, m, w) in enumerate(species):
         cfg.q[i], cfg.m[i], cfg.w[i] = q, m, w
         cfg.capacity[i] = 0 if capacity is None else int(capacity[i])
-    cfg.supercell, cfg.sort_every = supercell, sort_every
+    cfg.supercell, cfg.halo, cfg.sort_every = supercell, halo, sort_every
     cfg.rank, cfg.nranks, cfg.flags = rank, nranks, flags
     cfg.migrate_capacity = migrate_capacity
     if nccl_id is not None:
@@ -318,7 +319,8 @@ class Simulation:
 
 
 def workload_config(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
-                    sort_every=None, nccl_id=None, counts=None, migrate_capacity=0, slab=None):
+                    sort_every=None, nccl_id=None, counts=None, migrate_capacity=0, slab=None,
+                    halo=None):
     """pic_config for a synth.Workload (species q, m, w, dt, z boundary and
     laser from the workload).
 
@@ -345,15 +347,16 @@ def workload_config(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercel
                        wl.sort_every if sort_every is None else sort_every,
                        rank, nranks, flags, nccl_id, migrate_capacity,
                        bc_z=BC_OPEN if getattr(wl, "open_z", False) else BC_PERIODIC,
-                       slab=slab if nranks > 1 else None, laser=laser)
+                       slab=slab if nranks > 1 else None, laser=laser,
+                       halo=halo or getattr(wl, "halo", 1))
 
 
 def simulation_from_workload(wl, capacity_factor=1.0, flags=0, rank=0, nranks=1, supercell=None,
                              sort_every=None, nccl_id=None, counts=None, migrate_capacity=0,
-                             stream=None, slab=None):
+                             stream=None, slab=None, halo=None):
     """Build a Simulation for a synth.Workload."""
     cfg = workload_config(wl, capacity_factor, flags, rank, nranks, supercell, sort_every,
-                          nccl_id, counts, migrate_capacity, slab)
+                          nccl_id, counts, migrate_capacity, slab, halo)
     return Simulation(cfg, stream=stream)
 
 

@@ -53,6 +53,7 @@ class Workload:
     steps: int
     sort_every: int = 20
     supercell: int = 4
+    halo: int = 1               # tile drift halo h of the fused kernel (pic_config.halo)
     seed: int = 0
     dx: float = 1.0
     dy: float = 1.0

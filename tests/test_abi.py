@@ -86,11 +86,15 @@ def test_workspace_size_is_pure_and_validates(built):
     big = C.c_size_t(0)
     assert L.pic_workspace_size(C.byref(_cfg(capacity=[10 * 32768])), C.byref(big)) == 0
     assert big.value > nb.value
+    for h in (0, 1, 2):
+        assert L.pic_workspace_size(C.byref(_cfg(halo=h)), C.byref(big)) == 0
     bad = [
         _cfg(dt=0.6),                      # CFL: 1/sqrt(3) = 0.577
         _cfg(supercell=3),                 # does not divide 16
         _cfg(species=[(-1.0, 0.0, 1.0)]),  # zero mass
         _cfg(nx=0),
+        _cfg(halo=3),                      # tile drift halo h in {1, 2}
+        _cfg(halo=-1),
     ]
     for b in bad:
         assert L.pic_workspace_size(C.byref(b), C.byref(nb)) == -1

@@ -402,15 +402,18 @@ def _slab_group(pic, wl, nranks, stream):
     return sims
 
 
-@pytest.mark.parametrize("nranks", [2, 4])
-def test_slab_decomposition_matches_single_domain_oracle(pic, oracle_mod, nranks):
+@pytest.mark.parametrize("nranks,nz", [(2, 16), (4, 16), (2, 32)])
+def test_slab_decomposition_matches_single_domain_oracle(pic, oracle_mod, nranks, nz):
     """The z-slab path (J ghost planes summed by the owner, E/B ghost planes,
     particle migration, unsorted arrivals tail) run as an in-process group of
-    slab contexts on one GPU, against the single-domain oracle (P16)."""
+    slab contexts on one GPU, against the single-domain oracle (P16).  With
+    nz = 32 over 2 ranks each slab has 4 supercell layers: the step pushes
+    the boundary layers 0 and 3 first, exchanges, then the interior layers
+    1 and 2 (the overlap order of a NCCL step)."""
     import torch
     from synth import gen_particles, get_config
     from synth.configs import electron
-    wl = get_config("C1").with_(species=(electron(6, 0.2),), nz=16, sort_every=5)
+    wl = get_config("C1").with_(species=(electron(6, 0.2),), nz=nz, sort_every=5)
     parts = gen_particles(wl)
     rng = np.random.default_rng(21)
     F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.02
@@ -464,6 +467,35 @@ def test_supercell_two_tile_kernel(pic, oracle_mod):
     rng = np.random.default_rng(22)
     F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.05
     _run_parity(pic, oracle_mod, wl, 8, teacher_forced=False, fields=F6, tol=1e-11)
+
+
+@pytest.mark.parametrize("S", [4, 2])
+def test_halo_two_tile_kernel(pic, oracle_mod, S):
+    """Tile drift halo h = 2 (pic_config.halo; SURVEY.md sec. 8b "supercell
+    S, halo h"): (S + 6)^3 E/B and (S + 7)^3 J tiles -- at S = 4 one CTA of
+    512 threads per SM -- against the oracle, two species in one launch,
+    fast enough (sigma 0.3, no re-sort for 20 steps) that particles drift
+    past 1 and past 2 cells out of their supercell (tile and global paths)."""
+    from synth import get_config
+    from synth.configs import electron, proton
+    wl = get_config("C1").with_(species=(electron(3, 0.3), proton(2, 200.0)), sort_every=0,
+                                nx=16, ny=16, nz=8, supercell=S, halo=2)
+    rng = np.random.default_rng(40 + S)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.05
+    _run_parity(pic, oracle_mod, wl, 20, teacher_forced=False, fields=F6, tol=1e-10)
+
+
+def test_halo_two_c1_teacher_forced(pic, oracle_mod):
+    """C1 per step at h = 2 with the sort every 5 steps: <= 1e-12."""
+    from synth import get_config
+    wl = get_config("C1").with_(halo=2, sort_every=5)
+    _run_parity(pic, oracle_mod, wl, wl.steps, teacher_forced=True)
+
+
+def test_halo_rejected_out_of_range(pic):
+    with pytest.raises(pic.PicError):
+        cfg = pic.make_config(8, 8, 8, [(-1.0, 1.0, 1.0)], dt=0.25, capacity=[10], halo=3)
+        pic.Simulation(cfg)
 
 
 def test_dense_supercell_global_path(pic, oracle_mod):

@@ -14,11 +14,20 @@ from synth import gen_particles, get_config  # noqa: E402
 
 
 def main():
-    name, steps = sys.argv[1], int(sys.argv[2])
+    # WORKLOAD[:hH][:kK]  (halo / sort interval overrides, e.g. C3:h2:k40)
+    spec, steps = sys.argv[1], int(sys.argv[2])
+    name, *mods = spec.split(":")
     wl = get_config(name)
+    for m in mods:
+        if m[0] == "h":
+            wl = wl.with_(halo=int(m[1:]))
+        elif m[0] == "k":
+            wl = wl.with_(sort_every=int(m[1:]))
+        elif m[0] == "s":
+            wl = wl.with_(supercell=int(m[1:]))
     parts = gen_particles(wl)
     n = sum(p.shape[1] for p, _ in parts)
-    out = {"workload": name}
+    out = {"workload": spec}
     for flags in (0, pkg.FLAG_PROFILE):
         sim = pkg.simulation_from_workload(wl, capacity_factor=1.0, flags=flags)
         for s, (P, ids) in enumerate(parts):
