@@ -71,8 +71,7 @@ struct TileGeom {
     static constexpr size_t off_qcell = off_jt + 9 * NJ * sizeof(unsigned);    // [kQueue] u32
     static constexpr size_t off_fq = off_qcell + (kQueue + 1) * sizeof(unsigned);   // [kFQueue + 1] u32
     static constexpr size_t off_misc = (off_fq + (kFQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
-    static constexpr size_t smem_bytes = off_misc + 2 * sizeof(uint64_t);      // 1 mbarrier + the TMEM base
-    static constexpr int TMEM_COLS = 32 * (NT / 128);   // 24 used per warp, 4 warps share a lane quadrant
+    static constexpr size_t smem_bytes = off_misc + sizeof(uint64_t);          // 1 mbarrier
     static_assert(smem_bytes <= 227 * 1024, "tiles exceed shared memory");
 };
 
@@ -93,9 +92,6 @@ constexpr double kFixRange = 140737488355328.0;  // 2^47: |v| of one accumulated
 // (a particle adds to an edge at most 4 times), with a margin for the
 // floor of the accumulated flushes' high words
 constexpr int64_t kMaxTileParticles = 16000;
-#ifndef PIC_TMEM_ACC
-#define PIC_TMEM_ACC 0
-#endif
 
 // The 12 Villasenor-Buneman edge values of one in-cell segment P1 -> P2
 // (local coordinates of the segment's cell), times the flux
@@ -132,24 +128,6 @@ __device__ __forceinline__ EdgeVals seg_values(double p1x, double p1y, double p1
     return e;
 }
 
-// The 4 edge values of component d (0 = Jx, 1 = Jy, 2 = Jz) of seg_values,
-// with the scaled flux factor ks of that axis.
-__device__ __forceinline__ void seg_values_axis(int d, double p1x, double p1y, double p1z, double p2x, double p2y,
-                                                double p2z, double ks, double v[4])
-{
-    const double D[3] = {p2x - p1x, p2y - p1y, p2z - p1z};
-    const double M[3] = {0.5 * (p1x + p2x), 0.5 * (p1y + p2y), 0.5 * (p1z + p2z)};
-    // the two transverse axes, in the order of seg_values' edge list
-    const int a = d == 0 ? 1 : 0, b = d == 2 ? 1 : 2;
-    const double f = ks * D[d];
-    const double c = D[a] * D[b] * (1.0 / 12.0);
-    const double ma = M[a], mb = M[b], na = 1.0 - ma, nb = 1.0 - mb;
-    v[0] = f * fma(na, nb, c);
-    v[1] = f * fma(ma, nb, -c);
-    v[2] = f * fma(na, mb, -c);
-    v[3] = f * fma(ma, mb, c);
-}
-
 // J-tile offsets of the 12 edges of a cell (order of seg_values)
 template <class T>
 __device__ __forceinline__ constexpr int edge_off(int e)
@@ -174,49 +152,6 @@ __device__ __forceinline__ void fixed_add(unsigned *b, double vs)
     atomicAdd(b, lo & 0xffffu);
     atomicAdd(b + 3 * NJ, lo >> 16);
     atomicAdd(b + 6 * NJ, hi);
-}
-
-// Adds the exact integer v (|v| < 2^63) to a tile entry: lo16 | mid16 | hi.
-template <class T>
-__device__ __forceinline__ void fixed_add_int(unsigned *b, long long v)
-{
-    constexpr int NJ = T::NJ;
-    const unsigned lo = (unsigned)v;
-    atomicAdd(b, lo & 0xffffu);
-    atomicAdd(b + 3 * NJ, lo >> 16);
-    atomicAdd(b + 6 * NJ, (unsigned)(int)(v >> 32));
-}
-
-// Flushes a thread's accumulator (sums of n biased bit patterns, see the
-// kernel) into the 12 edges of the cell at jbase.
-template <class T>
-__device__ __forceinline__ void tile_add_acc(unsigned *jt, int jbase, const unsigned long long acc[12], unsigned n)
-{
-    const unsigned long long bias = (unsigned long long)n * 0x4338000000000000ull;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) fixed_add_int<T>(jt + jbase + edge_off<T>(k), (long long)(acc[k] - bias));
-}
-
-// the same from an accumulator held as 24 u32 words (lo, hi per value)
-template <class T>
-__device__ __forceinline__ void tile_add_acc_words(unsigned *jt, int jbase, const uint32_t w[24], unsigned n)
-{
-    const unsigned long long bias = (unsigned long long)n * 0x4338000000000000ull;
-#pragma unroll
-    for (int k = 0; k < 12; ++k)
-        fixed_add_int<T>(jt + jbase + edge_off<T>(k),
-                         (long long)((((unsigned long long)w[2 * k + 1] << 32) | w[2 * k]) - bias));
-}
-
-// component d's 4 values of an accumulator held as 8 u32 words
-template <class T>
-__device__ __forceinline__ void tile_add_acc_words4(unsigned *jt, int jbase, int d, const uint32_t w[8], unsigned n)
-{
-    const unsigned long long bias = (unsigned long long)n * 0x4338000000000000ull;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        fixed_add_int<T>(jt + jbase + edge_off<T>(4 * d + k),
-                         (long long)((((unsigned long long)w[2 * k + 1] << 32) | w[2 * k]) - bias));
 }
 
 template <class T>
@@ -330,7 +265,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     unsigned *fq = (unsigned *)(smem_raw + T::off_fq);     // particles outside the tile
     unsigned *fqcount = fq + kFQueue;
     uint64_t *bar_eb = (uint64_t *)(smem_raw + T::off_misc);
-    uint32_t *tmem_slot = (uint32_t *)(smem_raw + T::off_misc + sizeof(uint64_t));
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // `split` CTAs share a supercell, each taking a contiguous part of its
     // particles (short grids fill the last wave; each CTA has its own tiles)
@@ -356,9 +290,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     if (NSP == 2) range(1, a1, b1);
     const int n0 = b0 - a0, total = n0 + (b1 - a1);
     if (total == 0) return;   // empty (uniform per CTA)
-#if PIC_TMEM_ACC
-    if (wid == 0) tmem_alloc(tmem_slot, T::TMEM_COLS);   // read after the __syncthreads below
-#endif
     // concatenated index i -> species (s1: the second one) and its array index p
     auto locate = [&](int i, bool &s1, int &p) {
         s1 = NSP == 2 && i >= n0;
@@ -421,65 +352,23 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
         kmax = fmax(kmax, fmax(fabs(ts.sp[NSP - 1].kx), fmax(fabs(ts.sp[NSP - 1].ky), fabs(ts.sp[NSP - 1].kz))));
     const double dlim = fmin(1.0, kFixRange / (kmax * scale * (13.0 / 12.0)));
     const bool tile_ok = total <= kMaxTileParticles;   // else the counters could overflow
-#if PIC_TMEM_ACC
-    // Per-thread fixed-point accumulator of the first-piece edge values of the
-    // particles whose path starts in the cell acc_cell, kept in TENSOR MEMORY
-    // (TMEM, the per-SM 256 KB array of the 5th-generation tensor cores, here
-    // used as private per-thread storage: warp w owns TMEM lanes 32 (w % 4) ..
-    // and 24 columns at 32 (w / 4), one lane per thread).  It holds the raw
-    // bit patterns of v + 1.5*2^52 summed as u64 (mod 2^64; acc_n of them), so
-    // sum - acc_n * bits(1.5*2^52) is the exact integer sum of the rounded
-    // values and the tile ends up bit-identical to per-particle atomics.  The
-    // slot-major order keeps a thread on one cell of its supercell for as long
-    // as the cells' particle counts allow (always, for a species that does not
-    // move across cells), so those first pieces reach the shared tile -- 36
-    // atomics, each a read and a write wavefront of the shared-memory pipe,
-    // the kernel's binding resource -- once per cell change instead of once
-    // per particle; TMEM traffic does not use that pipe.
-#endif
-    tmem_fence_before_sync();
     __syncthreads();
-    tmem_fence_after_sync();
-#if PIC_TMEM_ACC
-    const uint32_t tmem_base = *tmem_slot;
-    unsigned acc_n = 0u;
-    int acc_cell = -1;
-    // warp w: TMEM lanes 32 (w % 4) .. + 31, columns 32 (w / 4) .. + 23
-    const uint32_t tacc = tmem_base + ((uint32_t)(32 * (wid & 3)) << 16) + 32u * (uint32_t)(wid >> 2);
-    {
-        uint32_t z[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) z[k] = 0u;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) tmem_st8(tacc + 8u * d, z);
-    }
-#endif
     mbar_wait(bar_eb, 0);
 
     int st = 0;
-    // warp-uniform trip count (the TMEM accumulator is updated by the whole
-    // warp every iteration): lanes past the end run the iteration idle
-    for (int i = tid; i - lane < total; i += NT) {
-        const bool valid = i < total;
+    for (int i = tid; i < total; i += NT) {
         if (i + NT < total) stage(i + NT, st ^ 1);   // prefetch the next particle
         cp_async_commit();
         cp_async_wait1();
         bool s1;
         int p;
-        locate(valid ? i : 0, s1, p);
+        locate(i, s1, p);
         const double *pl = pbuf + st * 6 * NT + tid;
         st ^= 1;
-        const double x = valid ? pl[0] : kDeadX, y = pl[NT], z = pl[2 * NT];
-#if PIC_TMEM_ACC
-        // first piece of this particle's path (start and end in its cell's
-        // coordinates) for the thread's accumulator, added after the branch
-        bool have = false, hs1 = false;
-        int jfirst = 0;
-        double fa0 = 0.0, fa1 = 0.0, fa2 = 0.0, fb0 = 0.0, fb1 = 0.0, fb2 = 0.0;
-#endif
+        const double x = pl[0], y = pl[NT], z = pl[2 * NT];
         // dead slot (migrated away or absorbed since the last sort; a single
-        // periodic box has none) or a lane past the end
-        if (valid && !(kGeneral && x < 0.0)) {
+        // periodic box has none)
+        if (kGeneral && x < 0.0) continue;
         double ux = pl[3 * NT], uy = pl[4 * NT], uz = pl[5 * NT];
         const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
         const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
@@ -533,23 +422,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                 int cx, cy, cz;
                 const bool more =
                     vb_first_piece(wx.f0, wy.f0, wz.f0, bxl, byl, bzl, ex_, ey_, ez_, r1, r2, cx, cy, cz);
-#if PIC_TMEM_ACC
-                PIC_DCHECK(jbase >= 0 && tx + 1 < T::TJ && ty + 1 < T::TJ && tz + 1 < T::TJ, err);
-                if (fits) {   // to the TMEM accumulator after the branch (warp-converged)
-                    have = true;
-                    hs1 = s1;
-                    jfirst = jbase;
-                    fa0 = wx.f0; fa1 = wy.f0; fa2 = wz.f0;
-                    fb0 = ex_; fb1 = ey_; fb2 = ez_;
-                } else {
-                    global_add<T>(J, gorigin, g, jbase,
-                                  seg_values(wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx * scale, ky * scale, kz * scale),
-                                  inv_scale);
-                }
-#else
                 deposit_seg<T>(jt, jbase, J, gorigin, g, wx.f0, wy.f0, wz.f0, ex_, ey_, ez_, kx, ky, kz, scale,
                                inv_scale, fits, err);
-#endif
                 if (more) {
                     // the rest of a face-crossing path is deposited after the particle
                     // loop, all queued paths together (keeps the loop convergent); the
@@ -568,17 +442,13 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                         qb = __shfl_sync(act, qb, leader);
                         if (fits) slot = qb + (unsigned)__popc(want & ((1u << lane) - 1u));
                     }
-                    // the remainder in the next cell's coordinates: r1 = e - o,
-                    // r2 = b - o (the same subtractions vb_first_piece makes)
-                    const double r10 = ex_ - (double)cx, r11 = ey_ - (double)cy, r12 = ez_ - (double)cz;
-                    const double r20 = bxl - (double)cx, r21 = byl - (double)cy, r22 = bzl - (double)cz;
                     if (slot < (unsigned)kQueue) {
-                        q[0 * kQueue + slot] = r10; q[1 * kQueue + slot] = r11; q[2 * kQueue + slot] = r12;
-                        q[3 * kQueue + slot] = r20; q[4 * kQueue + slot] = r21; q[5 * kQueue + slot] = r22;
+                        q[0 * kQueue + slot] = r1[0]; q[1 * kQueue + slot] = r1[1]; q[2 * kQueue + slot] = r1[2];
+                        q[3 * kQueue + slot] = r2[0]; q[4 * kQueue + slot] = r2[1]; q[5 * kQueue + slot] = r2[2];
                         qcell[slot] = (unsigned)jrem | (s1 ? 0x80000000u : 0u);
                     } else {
-                        deposit_remainder<T>(jt, jrem, J, gorigin, g, r10, r11, r12, r20, r21, r22, kx, ky, kz,
-                                             scale, inv_scale, fits, err);
+                        deposit_remainder<T>(jt, jrem, J, gorigin, g, r1[0], r1[1], r1[2], r2[0], r2[1],
+                                             r2[2], kx, ky, kz, scale, inv_scale, fits, err);
                     }
                 }
             } else {
@@ -603,55 +473,7 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
                 if (NSP == 2) u2hi1 = max(u2hi1, s1 ? h2 : 0u);
             }
         }
-        }   // live slot
-#if PIC_TMEM_ACC
-        // the whole warp, converged: accumulator += this particle's first piece
-        // (a cell change first flushes the old sums to the shared tile); in
-        // three passes of 8 TMEM columns (the 4 edges of Jx, Jy, Jz), which
-        // keeps the registers in flight low
-        __syncwarp();
-        {
-            const SpeciesDev &hsp = hs1 ? ts.sp[NSP - 1] : ts.sp[0];
-            const bool flush = have && jfirst != acc_cell && acc_n;
-            const bool reset = have && jfirst != acc_cell;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                uint32_t r[8];
-                tmem_ld8(tacc + 8u * d, r);
-                if (flush) tile_add_acc_words4<T>(jt, acc_cell, d, r, acc_n);
-                if (have) {
-                    double v4[4];
-                    seg_values_axis(d, fa0, fa1, fa2, fb0, fb1, fb2,
-                                    (d == 0 ? hsp.kx : d == 1 ? hsp.ky : hsp.kz) * scale, v4);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const unsigned long long old =
-                            reset ? 0ull : (((unsigned long long)r[2 * k + 1] << 32) | r[2 * k]);
-                        const unsigned long long v = old + (unsigned long long)__double_as_longlong(v4[k] + kMagic);
-                        r[2 * k] = (uint32_t)v;
-                        r[2 * k + 1] = (uint32_t)(v >> 32);
-                    }
-                }
-                __syncwarp();
-                tmem_st8(tacc + 8u * d, r);
-            }
-            if (reset) {
-                acc_cell = jfirst;
-                acc_n = 0u;
-            }
-            acc_n += have ? 1u : 0u;
-        }
-#endif
     }
-#if PIC_TMEM_ACC
-    __syncwarp();
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        uint32_t r[8];
-        tmem_ld8(tacc + 8u * d, r);
-        if (acc_n) tile_add_acc_words4<T>(jt, acc_cell, d, r, acc_n);
-    }
-#endif
     __syncthreads();   // all particles pushed, the queues are complete
     const int nq = min(*qcount, (unsigned)kQueue);
     for (int e = tid; e < nq; e += NT) {
@@ -708,12 +530,6 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
             }
         }
     }
-#if PIC_TMEM_ACC
-    tmem_fence_before_sync();
-    __syncthreads();   // every warp's TMEM traffic is done
-    tmem_fence_after_sync();
-    if (wid == 0) tmem_dealloc(tmem_base, T::TMEM_COLS);
-#endif
 }
 
 __global__ void __launch_bounds__(256) k_u2max(ParticlesDev P, int64_t n, unsigned *out)

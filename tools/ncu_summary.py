@@ -21,7 +21,11 @@ want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "launch__registers_
         "dram__bytes_read.sum", "dram__bytes_write.sum",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts.sum", "l1tex__data_pipe_lsu_wavefronts_cmd_read.sum",
+        "l1tex__data_pipe_lsu_wavefronts_cmd_write.sum",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum"]
 for w in want:
     print(w.ljust(78), d.get(w))
 st = [(h, v) for h, v in zip(hdr, vals) if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")]
