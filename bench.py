@@ -256,6 +256,24 @@ def host_info():
     return host
 
 
+def data_pipe_roof(ncu, launch_ms, sm_mhz):
+    """The binding resource of the fused particle kernel:
+    the SM's L1/shared-memory data pipe, one 128-byte wavefront per SM clock
+    for every LDS, STS, ATOMS (a read and a write wavefront), LDGSTS fill,
+    global load/store and local spill.  achieved = the ncu-counted wavefronts
+    of one launch (profiles/ncu_particle_traffic.json, the commit it was
+    captured at) over this run's launch time; peak = 148 SMs x the SM clock
+    sampled under load."""
+    w = ncu.get("lsu_wavefronts_per_launch")
+    if not w or not sm_mhz:
+        return None
+    peak = 148 * sm_mhz * 1e6
+    achieved = w / (launch_ms * 1e-3)
+    return {"unit": "wavefronts/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+            "wavefronts_per_launch": w, "source": f"ncu l1tex__data_pipe_lsu_wavefronts.sum at commit "
+                                                  f"{ncu.get('commit', '?')}; peak = 148 SM x {sm_mhz:.0f} MHz"}
+
+
 def fp64_roof(rate_per_gpu, flop_upd, ncu, peak, peak_src):
     """The FP64 roof of SURVEY.md sec. 8d from this kernel's own counted work
     per update (ncu opcode mix of the captured launch, null if none), with
@@ -473,6 +491,8 @@ def run_ours(args, wl, rank, world, local):
                          f"{wl.name} (whole grid), {dt:.1f} s, single thread",
                "host": host_info()}
 
+    csum = clk.summary()
+    clk_mhz_hint = csum.get("sm_mhz") or csum.get("sm_max_mhz")
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -500,12 +520,13 @@ def run_ours(args, wl, rank, world, local):
                                              + n_cells_local * 120.0)
                          / (t_ms * 1e-3 / args.steps) / 1e9 / peak,
                          # the second roof (report both fractions)
-                         "fp64": fp64_roof(value / world, flop_upd, ncu, fp64_peak, fp64_src)},
+                         "fp64": fp64_roof(value / world, flop_upd, ncu, fp64_peak, fp64_src),
+                         "data_pipe": data_pipe_roof(ncu, per_launch_ms, clk_mhz_hint)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "stage_ms_per_step_by_rank": by_rank,
-            "clocks": clk.summary(),
+            "clocks": csum,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -6,7 +6,8 @@ bench.py's roofline):
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,\
 smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,\
 smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,\
-smsp__sass_thread_inst_executed_op_dmul_pred_on.sum \
+smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,\
+l1tex__data_pipe_lsu_wavefronts.sum \
         --clock-control none -k regex:k_push_tile -s 3 -c 1 --csv \
         python tools/run_steps.py C3 6 > gpurun_out/ncu_counts_C3.csv
     python tools/ncu_counts.py C3 gpurun_out/ncu_counts_C3.csv COMMIT
@@ -66,6 +67,9 @@ def main():
         "fp64_flop_per_launch": flop,
         "fp64_flop_per_update": flop / n,
     }
+    if "l1tex__data_pipe_lsu_wavefronts.sum" in m:
+        # the L1/shared-memory data pipe: one 128-byte wavefront per SM clock
+        data[wl_name]["lsu_wavefronts_per_launch"] = m["l1tex__data_pipe_lsu_wavefronts.sum"]
     json.dump(data, open(p, "w"), indent=1)
     print(json.dumps(data[wl_name], indent=1))
 
