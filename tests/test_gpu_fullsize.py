@@ -104,3 +104,40 @@ def test_c3_whole_state_one_step(pic, oracle_mod):
     errs = _errors(sim, orc, wl)
     _report("C3", 1, errs)
     assert max(errs.values()) <= TOL_STEP, errs
+
+
+def test_c5_1g_whole_state_one_step(pic, oracle_mod):
+    """C5_1g (128 x 128 x 1024 open-z box, the incident laser preloaded up to
+    the slab, 52.4M electrons + 52.4M co-located protons in one launch) with
+    the electrons' momenta drawn hot (sigma 1 m_e c: gamma up to ~5) so the
+    open-box store, the Mur faces, the laser injection and relativistic
+    pushes and deposits all act in one step from the common state: every
+    array <= 1e-12 of its own maximum (none is symmetry-zero here: the
+    thermal currents fill all three components)."""
+    from dataclasses import replace
+    from synth import gen_particles, get_config
+    base = get_config("C5_1g")
+    e, p = base.species
+    wl = base.with_(species=(replace(e, sigma_p=1.0), p))
+    parts = gen_particles(wl)
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    sim.laser_preload()
+    sim.step(1)
+    lz = dict(wl.laser)
+    O = oracle_mod
+    g = O.Grid(wl.nx, wl.ny, wl.nz, wl.dx, wl.dy, wl.dz, wl.dt, wl.c,
+               [O.Species(s.q, s.m, s.w) for s in wl.species], wl.supercell, wl.sort_every,
+               bc_z=O.BC_OPEN, laser_e0=lz["e0"], laser_omega=lz["omega"], laser_ramp=lz["ramp"],
+               laser_t0=lz["t0"], laser_pol=tuple(lz["pol"]))
+    orc = O.Oracle(g, particles=parts)
+    del parts
+    orc.laser_preload()
+    t0 = time.perf_counter()
+    orc.step(1)
+    print(f"C5_1g oracle step {time.perf_counter() - t0:.1f} s", flush=True)
+    errs = _errors(sim, orc, wl)
+    _report("C5_1g", 1, errs)
+    assert max(errs.values()) <= TOL_STEP, errs
+    assert np.abs(orc.P[0][3:]).max() > 3.0   # relativistic electrons
