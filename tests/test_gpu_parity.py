@@ -118,6 +118,31 @@ def test_sort_order_kernel_paths(pic, oracle_mod, case):
     assert np.array_equal(np.sort(gids2), np.sort(ids))
 
 
+@pytest.mark.parametrize("S,K", [(4, 3), (2, 2)])
+def test_in_step_sort_order_bit_exact(pic, oracle_mod, S, K):
+    """The sorts inside the step (of the store the pushes left, as opposed to
+    the host input pic_set_particles sorts) give the oracle's permutation bit
+    for bit after every re-sort: the particle order of the GPU store equals
+    the oracle's array order (both sort at the start of steps n = 0, K, 2K,
+    ...; fast particles, sigma 0.3, so many change supercell between sorts)."""
+    from synth import get_config, gen_particles
+    from synth.configs import electron
+    wl = get_config("C1").with_(species=(electron(5, 0.3),), supercell=S, sort_every=K)
+    parts = gen_particles(wl)
+    orc = _oracle_for(oracle_mod, wl, parts)
+    sim = _sim(pic, wl)
+    _load(sim, parts)
+    orc.sort()
+    for step in range(3 * K + 1):
+        orc.step(1)
+        sim.step(1)
+        if step % K == 0:   # this step began with a sort
+            gP, gids = sim.get_particles(0)
+            assert np.array_equal(gids, orc.ids[0]), step
+            L = _L(wl)
+            assert pos_err(gP[:3], orc.P[0][:3], L) <= TOL_STEP
+
+
 # ---------------------------------------------------------------- fields (a7)
 
 def test_fdtd_random_fields_vs_oracle(pic, oracle_mod):
