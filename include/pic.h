@@ -141,6 +141,11 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n,
  * order Ex,Ey,Ez,Bx,By,Bz; Yee-staggered as in DESIGN.md sec. 4). */
 int pic_set_fields(pic_ctx *ctx, const double *f);
 
+/* The same with one HOST pointer per component (SURVEY.md sec. 8b's
+ * pic_set_fields(ctx, const double* const f[6])): f[c] is [nz_local][ny][nx],
+ * c = Ex,Ey,Ez,Bx,By,Bz.  PIC_EINVAL for a NULL component. */
+int pic_set_fields6(pic_ctx *ctx, const double *const f[6]);
+
 /* Advances nsteps time steps (per step: a1 sort when
  * step % K == 0; a2-a6 fused gather/push/deposit per species; a7 Yee
  * update; a8 exchange when nranks > 1).  Synchronises cfg->stream at the
@@ -174,6 +179,11 @@ int pic_step_group(pic_ctx *const *ctxs, int n, int64_t nsteps);
  * step) of the local slab without ghosts into a HOST array
  * f[9][nz_local][ny][nx] (Ex,Ey,Ez,Bx,By,Bz,Jx,Jy,Jz). */
 int pic_get_fields(pic_ctx *ctx, double *f);
+
+/* The same into one HOST pointer per component (SURVEY.md sec. 8b's
+ * pic_get_fields(ctx, double* const f[9])), c = Ex,Ey,Ez,Bx,By,Bz,Jx,Jy,Jz;
+ * a NULL component is skipped. */
+int pic_get_fields9(pic_ctx *ctx, double *const f[9]);
 
 /* Copies the live particles of `species` in their current device order
  * (sorted region, then particles received since the last sort) to HOST arrays.  *n_inout: capacity of the arrays in, particle count out

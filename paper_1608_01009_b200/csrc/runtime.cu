@@ -1057,14 +1057,15 @@ int pic_set_particles(pic_ctx *ctx, int species, int64_t n, const double *x, con
     return check_device_error(ctx);
 }
 
-int pic_set_fields(pic_ctx *ctx, const double *f)
+int pic_set_fields6(pic_ctx *ctx, const double *const f[6])
 {
     if (!ctx || !f) return PIC_EINVAL;
+    for (int c = 0; c < 6; ++c)
+        if (!f[c]) return fail(ctx, PIC_EINVAL, "pic_set_fields6: NULL component");
     const GridDev &g = ctx->L.g;
     for (int c = 0; c < 6; ++c) {
         cudaMemcpy3DParms p = {};
-        p.srcPtr = make_cudaPitchedPtr((void *)(f + (size_t)c * g.nx * g.ny * g.nz),
-                                       sizeof(double) * g.nx, g.nx, g.ny);
+        p.srcPtr = make_cudaPitchedPtr((void *)f[c], sizeof(double) * g.nx, g.nx, g.ny);
         p.dstPtr = make_cudaPitchedPtr(ctx->EB + c * g.cs, sizeof(double) * g.X, g.X, g.Y);
         p.dstPos = make_cudaPos(sizeof(double) * kGhost, kGhost, kGhost);
         p.extent = make_cudaExtent(sizeof(double) * g.nx, g.ny, g.nz);
@@ -1080,23 +1081,41 @@ int pic_set_fields(pic_ctx *ctx, const double *f)
     return PIC_OK;
 }
 
-int pic_get_fields(pic_ctx *ctx, double *f)
+int pic_set_fields(pic_ctx *ctx, const double *f)
+{
+    if (!ctx || !f) return PIC_EINVAL;
+    const GridDev &g = ctx->L.g;
+    const size_t n = (size_t)g.nx * g.ny * g.nz;
+    const double *const comp[6] = {f, f + n, f + 2 * n, f + 3 * n, f + 4 * n, f + 5 * n};
+    return pic_set_fields6(ctx, comp);
+}
+
+int pic_get_fields9(pic_ctx *ctx, double *const f[9])
 {
     if (!ctx || !f) return PIC_EINVAL;
     const GridDev &g = ctx->L.g;
     for (int c = 0; c < 9; ++c) {
+        if (!f[c]) continue;
         const double *srcbase = c < 6 ? ctx->EB + c * g.cs : ctx->J[ctx->jlast] + (c - 6) * g.cs;
         cudaMemcpy3DParms p = {};
         p.srcPtr = make_cudaPitchedPtr((void *)srcbase, sizeof(double) * g.X, g.X, g.Y);
         p.srcPos = make_cudaPos(sizeof(double) * kGhost, kGhost, kGhost);
-        p.dstPtr = make_cudaPitchedPtr(f + (size_t)c * g.nx * g.ny * g.nz, sizeof(double) * g.nx,
-                                       g.nx, g.ny);
+        p.dstPtr = make_cudaPitchedPtr(f[c], sizeof(double) * g.nx, g.nx, g.ny);
         p.extent = make_cudaExtent(sizeof(double) * g.nx, g.ny, g.nz);
         p.kind = cudaMemcpyDeviceToHost;
         PIC_CUDA(ctx, cudaMemcpy3DAsync(&p, ctx->st));
     }
     PIC_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return PIC_OK;
+}
+
+int pic_get_fields(pic_ctx *ctx, double *f)
+{
+    if (!ctx || !f) return PIC_EINVAL;
+    const GridDev &g = ctx->L.g;
+    const size_t n = (size_t)g.nx * g.ny * g.nz;
+    double *const comp[9] = {f, f + n, f + 2 * n, f + 3 * n, f + 4 * n, f + 5 * n, f + 6 * n, f + 7 * n, f + 8 * n};
+    return pic_get_fields9(ctx, comp);
 }
 
 static int device_slots(pic_ctx *ctx, int species, int64_t *n)

@@ -32,7 +32,7 @@ EXPORTS = [
     "pic_get_fields", "pic_get_particles", "pic_get_count", "pic_get_step_index",
     "pic_get_stage_times", "pic_get_launch_count", "pic_strerror", "pic_last_error",
     "pic_destroy", "pic_nccl_unique_id", "pic_step_group", "pic_diagnostics",
-    "pic_diagnostics_group", "pic_laser_preload", "pic_balance_slabs",
+    "pic_diagnostics_group", "pic_laser_preload", "pic_balance_slabs", "pic_set_fields6", "pic_get_fields9",
 ]
 
 
@@ -127,6 +127,8 @@ def lib():
         L.pic_init.argtypes = [cp, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
         L.pic_set_particles.argtypes = [C.c_void_p, C.c_int, C.c_int64, dp, dp, dp, dp, dp, dp, u64p]
         L.pic_set_fields.argtypes = [C.c_void_p, dp]
+        L.pic_set_fields6.argtypes = [C.c_void_p, C.POINTER(dp)]
+        L.pic_get_fields9.argtypes = [C.c_void_p, C.POINTER(dp)]
         L.pic_step.argtypes = [C.c_void_p, C.c_int64]
         L.pic_get_fields.argtypes = [C.c_void_p, dp]
         L.pic_get_particles.argtypes = [C.c_void_p, C.c_int, i64p, dp, dp, dp, dp, dp, dp, u64p]
@@ -248,6 +250,20 @@ class Simulation:
         f6 = np.ascontiguousarray(f6, dtype=np.float64)
         assert f6.size == 6 * self.nx * self.ny * self.nz_local
         self._check(lib().pic_set_fields(self.ctx, _dptr(f6)))
+
+    def set_fields_components(self, comps):
+        """pic_set_fields6: six host arrays (Ex, Ey, Ez, Bx, By, Bz), each [nz_local][ny][nx]."""
+        arrs = [np.ascontiguousarray(c, dtype=np.float64) for c in comps]
+        assert len(arrs) == 6 and all(a.size == self.nx * self.ny * self.nz_local for a in arrs)
+        ptrs = (C.POINTER(C.c_double) * 6)(*[_dptr(a) for a in arrs])
+        self._check(lib().pic_set_fields6(self.ctx, ptrs))
+
+    def get_fields_components(self, which=range(9)):
+        """pic_get_fields9: the listed components (0..8 = Ex..Bz, Jx..Jz) as separate arrays."""
+        out = {c: np.empty((self.nz_local, self.ny, self.nx), dtype=np.float64) for c in which}
+        ptrs = (C.POINTER(C.c_double) * 9)(*[_dptr(out[c]) if c in out else None for c in range(9)])
+        self._check(lib().pic_get_fields9(self.ctx, ptrs))
+        return out
 
     def step(self, n=1):
         self._check(lib().pic_step(self.ctx, int(n)))

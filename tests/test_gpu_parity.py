@@ -163,6 +163,31 @@ def test_fdtd_random_fields_vs_oracle(pic, oracle_mod):
     assert not G[6:].any()
 
 
+def test_per_component_field_entry_points(pic):
+    """pic_set_fields6 / pic_get_fields9 (SURVEY.md sec. 8b's f[6] / f[9]
+    signatures) agree bit for bit with the packed pic_set_fields /
+    pic_get_fields, including after steps with particles (J)."""
+    from synth import get_config, gen_particles
+    wl = get_config("T_small")
+    rng = np.random.default_rng(19)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.05
+    a, b = _sim(pic, wl), _sim(pic, wl)
+    parts = gen_particles(wl)
+    _load(a, parts)
+    _load(b, parts)
+    a.set_fields(F6)
+    b.set_fields_components([F6[c] for c in range(6)])
+    assert np.array_equal(a.get_fields()[:6], F6)
+    a.step(3)
+    b.step(3)
+    G = a.get_fields()
+    comps = b.get_fields_components()
+    for c in range(9):
+        assert np.allclose(comps[c], G[c], rtol=0, atol=1e-13 * max(np.abs(G[c]).max(), 1e-300)), c
+    only = a.get_fields_components([6, 8])
+    assert sorted(only) == [6, 8] and np.array_equal(only[8], G[8])
+
+
 def test_vacuum_plane_wave_on_gpu(pic):
     # discrete Yee eigenmode along z, E along x (closed form, SURVEY P7)
     from synth import get_config
