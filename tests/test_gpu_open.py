@@ -145,6 +145,24 @@ def test_laser_plasma_free_running(pic, oracle_mod):
     print(f"free-running worst relative error {worst:.2e}")
 
 
+def test_laser_plasma_halo_two(pic, oracle_mod):
+    """The open box with the h = 2 tiles: T_laser free running 12 steps with
+    sorts (K = 5) against the oracle."""
+    from synth import gen_particles, get_config
+    wl = get_config("T_laser").with_(halo=2)
+    parts = gen_particles(wl)
+    orc = _oracle(oracle_mod, wl, parts)
+    orc.laser_preload()
+    sim = pic.simulation_from_workload(wl, capacity_factor=1.0)
+    for s, (P, ids) in enumerate(parts):
+        sim.set_particles(s, P, ids)
+    sim.laser_preload()
+    for step in range(12):
+        orc.step(1)
+        sim.step(1)
+        _check(sim, orc, wl, 1e-10, step)
+
+
 @pytest.mark.parametrize("where", ["bottom", "top"])
 def test_absorption_on_gpu(pic, oracle_mod, where):
     """Fast particles crossing the open faces are removed (the others keep

@@ -492,6 +492,41 @@ def test_slab_decomposition_matches_single_domain_oracle(pic, oracle_mod, nranks
     assert migrated > 0
 
 
+@pytest.mark.parametrize("S", [4, 2])
+def test_slab_decomposition_halo_two(pic, oracle_mod, S):
+    """The z-slab path with the h = 2 tiles (S = 4: one 512-thread CTA per
+    SM) and the boundary/interior split (2 slabs of 16 planes), two species
+    at sigma 0.3 drifting out of the sorted order between K = 5 sorts,
+    against the single-domain oracle."""
+    import torch
+    from synth import gen_particles, get_config
+    from synth.configs import electron, proton
+    wl = get_config("C1").with_(species=(electron(3, 0.3), proton(2, 200.0)), nz=32, sort_every=5,
+                                supercell=S, halo=2)
+    parts = gen_particles(wl)
+    rng = np.random.default_rng(24)
+    F6 = rng.standard_normal((6, wl.nz, wl.ny, wl.nx)) * 0.02
+    orc = _oracle_for(oracle_mod, wl, parts)
+    orc.F[:6] = F6
+    stream = torch.cuda.Stream()
+    sims = [pic.Simulation(pic.workload_config(wl, rank=r, nranks=2, flags=pic.FLAG_LOCAL_GROUP,
+                                               migrate_capacity=4096), stream=stream) for r in range(2)]
+    for r, sim in enumerate(sims):
+        for sp, (P, ids) in enumerate(parts):
+            sim.set_particles(sp, P, ids)
+        sim.set_fields(F6[:, r * 16:(r + 1) * 16].copy())
+    L = _L(wl)
+    for step in range(12):
+        orc.step(1)
+        pic.step_group(sims, 1)
+        G = np.concatenate([s.get_fields() for s in sims], axis=1)
+        errs = field_errs(G, orc.F)
+        for sp in range(2):
+            Ps, Is = zip(*[sim.get_particles(sp) for sim in sims])
+            errs += list(compare_state(np.concatenate(Ps, axis=1), np.concatenate(Is), orc.P[sp], orc.ids[sp], L))
+        assert max(errs) <= 1e-11, (step, errs)
+
+
 def test_slab_migration_capacity_error(pic):
     import torch
     from synth import gen_particles, get_config
