@@ -80,7 +80,13 @@ void configure_tile_kernels();
 // The species of one fused-kernel launch (one or two species with particles):
 // input arrays (sorted B on a sort step, else A), output arrays (A), offsets.
 constexpr int kTileMaxSpecies = 2;
+// the fused kernel stages a warp's 32 particles with one 2-D TMA load of a
+// [6 components][kPartBox particles] box of the SoA store (runtime.cu
+// encode_particle_maps): 34 = 32 + the one-node shift to an even (16-byte
+// aligned) start
+constexpr int kPartBox = 34;
 struct TileSpecies {
+    CUtensorMap pm[kTileMaxSpecies];   // TMA descriptors of the `in` stores
     ParticlesDev in[kTileMaxSpecies], out[kTileMaxSpecies];
     const int64_t *sc_off[kTileMaxSpecies];
     SpeciesDev sp[kTileMaxSpecies];

@@ -61,17 +61,22 @@ struct TileGeom {
     static_assert(EPX >= TE + XSH && JPX >= TJ && JPY >= JPX * TJ, "pitches");
     static_assert((EPX * 8) % 16 == 0, "TMA box row must be a multiple of 16 bytes");
     static constexpr size_t tiles = 6 * NE * sizeof(double) + 9 * NJ * sizeof(unsigned);
-    static constexpr int CTAS = tiles + 6 * kQueue * sizeof(double) + 12 * 256 * sizeof(double) < 110 * 1024 ? 2 : 1;
+    static constexpr int CTAS = tiles + 6 * kQueue * sizeof(double) + 12 * 288 * sizeof(double) < 110 * 1024 ? 2 : 1;
     static constexpr int NT = CTAS == 2 ? 256 : 512;   // threads per CTA
+    static constexpr int NW = NT / 32;                 // warps per CTA
+    static constexpr int PW = kPartBox;                // a warp's staged chunk: [6][PW] fp64 (one TMA box)
+    // fp64 per stage: the [6][PW] box, then the stage's mbarrier, 128-byte aligned stages
+    static constexpr int PSTAGE = (6 * PW * 8 + 8 + 127) / 128 * 16;
+    static constexpr int PBAR = 6 * PW * 8;   // byte offset of a stage's mbarrier
     // shared-memory layout (byte offsets, 128-B aligned where TMA writes)
     static constexpr size_t off_eb = 0;                                        // [6][NE] fp64
-    static constexpr size_t off_part = off_eb + 6 * NE * sizeof(double);       // [2][6][threads] fp64
-    static constexpr size_t off_q = off_part + 12 * NT * sizeof(double);       // [6][kQueue] fp64
+    static constexpr size_t off_part = off_eb + 6 * NE * sizeof(double);       // [NW][2][PSTAGE] fp64
+    static constexpr size_t off_q = off_part + NW * 2 * PSTAGE * sizeof(double);   // [6][kQueue] fp64
     static constexpr size_t off_jt = off_q + 6 * kQueue * sizeof(double);      // [9][NJ] u32
     static constexpr size_t off_qcell = off_jt + 9 * NJ * sizeof(unsigned);    // [kQueue] u32
     static constexpr size_t off_fq = off_qcell + (kQueue + 1) * sizeof(unsigned);   // [kFQueue + 1] u32
     static constexpr size_t off_misc = (off_fq + (kFQueue + 1) * sizeof(unsigned) + 15) / 16 * 16;
-    static constexpr size_t smem_bytes = off_misc + sizeof(uint64_t);          // 1 mbarrier
+    static constexpr size_t smem_bytes = off_misc + sizeof(uint64_t);         // the E/B tile's mbarrier
     static_assert(smem_bytes <= 227 * 1024, "tiles exceed shared memory");
 };
 
@@ -257,7 +262,8 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *eb = (double *)(smem_raw + T::off_eb);         // [6][TE][TE][EPX]
     const double *ebx = eb + T::XSH;                       // node (ox, oy, oz) of component 0
-    double *pbuf = (double *)(smem_raw + T::off_part);     // [2 stages][6][NT]
+    constexpr int PW = T::PW;
+    double *pbuf = (double *)(smem_raw + T::off_part) + (threadIdx.x >> 5) * 2 * T::PSTAGE;   // this warp's 2 stages
     double *q = (double *)(smem_raw + T::off_q);           // [6][kQueue]
     unsigned *jt = (unsigned *)(smem_raw + T::off_jt);     // [3 chunks][3][TJ][JPY/..]
     unsigned *qcell = (unsigned *)(smem_raw + T::off_qcell);
@@ -288,39 +294,52 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     int a0, b0, a1 = 0, b1 = 0;
     range(0, a0, b0);
     if (NSP == 2) range(1, a1, b1);
-    const int n0 = b0 - a0, total = n0 + (b1 - a1);
-    if (total == 0) return;   // empty (uniform per CTA)
-    // concatenated index i -> species (s1: the second one) and its array index p
-    auto locate = [&](int i, bool &s1, int &p) {
-        s1 = NSP == 2 && i >= n0;
-        p = s1 ? a1 + (i - n0) : a0 + i;
+    const int n0 = b0 - a0, n1 = b1 - a1;
+    if (n0 + n1 == 0) return;   // empty (uniform per CTA)
+    // concatenated index i: species 0 in [0, n0), species 1 from the next
+    // warp boundary n0p on (a warp's 32 particles are of one species); lanes
+    // in [n0, n0p) idle like the lanes past the end
+    const int n0p = NSP == 2 ? (n0 + 31) & ~31 : n0, total = n0p + n1;
+    const int a1m = a1 - n0p;   // species 1: array index = a1m + i (n0p even: same parity as a1)
+    auto locate = [&](int i, bool &s1, int &p) {   // -> species (s1: the second one), array index p
+        s1 = NSP == 2 && i >= n0p;
+        p = (s1 ? a1m : a0) + i;
     };
 
     // local-grid coordinates of the tile origin (same for the E/B and J tiles)
     const int ox = scx * S - H - 1, oy = scy * S - H - 1, oz = scz * S - H - 1;
     const int64_t gorigin = pidx(g, ox, oy, oz);   // padded global index of tile node (0,0,0)
 
+    // The particle state is staged through shared memory by the TMA engine:
+    // each warp stages the 32 particles of its iteration after next with one
+    // 2-D tensor load (the [6][kPartBox] box of the SoA store from the even
+    // node at or before its first particle) into one of its two stages,
+    // completing on the stage's mbarrier.  Per-thread LDGSTS staging costs
+    // ~19 more L1/shared data-pipe wavefronts per 32 particles -- the
+    // kernel's binding resource (tools/mb_stage.cu); per-warp stages keep the
+    // warps independent.
+    auto chunk_p = [&](int base, bool &s1) {   // array index of the warp chunk at concatenated index base
+        s1 = NSP == 2 && base >= n0p;
+        return (s1 ? a1m : a0) + base;
+    };
+    // shared-window address of the warp's stages; stage st's mbarrier sits
+    // at sbuf + st * PSTAGE * 8 + PBAR
+    const uint32_t sbuf = smem_u32(pbuf);
+    auto issue = [&](int base, int st) {   // lane 0
+        bool s1;
+        const int p = chunk_p(base, s1);
+        const uint32_t sdst = sbuf + st * (T::PSTAGE * 8u);
+        mbar_arrive_expect_tx(sdst + T::PBAR, 6 * kPartBox * sizeof(double));
+        tma_load_2d(sdst, s1 ? &ts.pm[NSP - 1] : &ts.pm[0], p & ~1, 0, sdst + T::PBAR);
+    };
     if (tid == 0) {
         mbar_init(bar_eb, 1);
+        for (int w = 0; w < 2 * T::NW; ++w)
+            mbar_init((uint64_t *)(smem_raw + T::off_part + w * (T::PSTAGE * 8) + T::PBAR), 1);
         fence_mbar_init();
         mbar_arrive_expect_tx(bar_eb, 6 * NE * sizeof(double));
         tma_load_4d(eb, &eb_map, ox + kGhost - T::XSH, oy + kGhost, oz + kGhost, 0, bar_eb);
     }
-    auto stage = [&](int i, int st) {   // this thread's particle i -> its staging slot
-        bool s1;
-        int p;
-        locate(i, s1, p);
-        const ParticlesDev &in = s1 ? ts.in[NSP - 1] : ts.in[0];
-        double *d = pbuf + st * 6 * NT + tid;
-        cp_async8(d + 0 * NT, in.x + p);
-        cp_async8(d + 1 * NT, in.y + p);
-        cp_async8(d + 2 * NT, in.z + p);
-        cp_async8(d + 3 * NT, in.ux + p);
-        cp_async8(d + 4 * NT, in.uy + p);
-        cp_async8(d + 5 * NT, in.uz + p);
-    };
-    if (tid < total) stage(tid, 0);
-    cp_async_commit();
     {   // zero the fixed-point J tile (16-byte stores)
         uint4 *j4 = (uint4 *)jt;
         for (int t = tid; t < (9 * NJ) / 4; t += NT) j4[t] = make_uint4(0u, 0u, 0u, 0u);
@@ -351,30 +370,41 @@ k_push_tile(const __grid_constant__ CUtensorMap eb_map, GridDev g, const double 
     if (NSP == 2)
         kmax = fmax(kmax, fmax(fabs(ts.sp[NSP - 1].kx), fmax(fabs(ts.sp[NSP - 1].ky), fabs(ts.sp[NSP - 1].kz))));
     const double dlim = fmin(1.0, kFixRange / (kmax * scale * (13.0 / 12.0)));
-    const bool tile_ok = total <= kMaxTileParticles;   // else the counters could overflow
-    __syncthreads();
+    const bool tile_ok = n0 + n1 <= kMaxTileParticles;   // else the counters could overflow
+    __syncthreads();   // mbarriers initialised, J tile zeroed
+    if (lane == 0) {   // this warp's first two chunks
+        if (tid < total) issue(tid, 0);
+        if (tid + NT < total) issue(tid + NT, 1);
+    }
     mbar_wait(bar_eb, 0);
 
-    int st = 0;
     // warp-uniform trip count: lanes past the end run the last iteration idle
     // (measured 4% faster on C3 than a per-lane loop: ptxas keeps the
     // two-species kernel at 128 registers without the spill the other form
     // has)
-    for (int i = tid; i - lane < total; i += NT) {
+    int c = 0;
+    for (int i = tid; i - lane < total; i += NT, ++c) {
         const bool valid = i < total;
-        if (i + NT < total) stage(i + NT, st ^ 1);   // prefetch the next particle
-        cp_async_commit();
-        cp_async_wait1();
+        const int st = c & 1;
+        mbar_wait(sbuf + st * (T::PSTAGE * 8u) + T::PBAR, (c >> 1) & 1);
+        // the chunk's first particle sits at slot 0 or 1 (its array index is
+        // a0 or a1 plus an even offset)
+        const double *pl = pbuf + st * T::PSTAGE + lane + ((NSP == 2 && i - lane >= n0p ? a1m : a0) & 1);
+        const double x0 = pl[0], y = pl[PW], z = pl[2 * PW];
+        double ux = pl[3 * PW], uy = pl[4 * PW], uz = pl[5 * PW];
+        __syncwarp();
+        if (lane == 0 && i - lane + 2 * NT < total) {   // refill the stage two iterations ahead
+            fence_proxy_async_smem();
+            issue(i - lane + 2 * NT, st);
+        }
         bool s1;
         int p;
         locate(valid ? i : 0, s1, p);
-        const double *pl = pbuf + st * 6 * NT + tid;
-        st ^= 1;
-        const double x = valid ? pl[0] : kDeadX, y = pl[NT], z = pl[2 * NT];
+        const bool live = valid && (NSP == 1 || i < n0 || i >= n0p);
+        const double x = live ? x0 : kDeadX;
         // dead slot (migrated away or absorbed since the last sort; a single
         // periodic box has none) or a lane past the end
-        if (!valid || (kGeneral && x < 0.0)) continue;
-        double ux = pl[3 * NT], uy = pl[4 * NT], uz = pl[5 * NT];
+        if (!live || (kGeneral && x < 0.0)) continue;
         const double gx = x * g.inv_dx, gy = y * g.inv_dy, gz = z * g.inv_dz - (double)g.k0;
         const AxisW wx = axis_weights(gx), wy = axis_weights(gy), wz = axis_weights(gz);
         // tile-relative start cell; inside the tile when in [1, S + 2H] on every axis

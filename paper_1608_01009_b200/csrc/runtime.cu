@@ -190,10 +190,14 @@ Layout make_layout(const pic_config *c)
     return L;
 }
 
+// bytes per SoA column of a particle store (+16: a staged chunk may read
+// up to 2 nodes past the last particle)
+static size_t particle_col_bytes(int64_t cap) { return align_up(sizeof(double) * (size_t)cap + 16); }
+
 ParticlesDev carve_particles(char *base, size_t off, int64_t cap)
 {
     ParticlesDev p;
-    const size_t col = align_up(sizeof(double) * (size_t)cap + 16);   // +16: a chunk may read 1 past
+    const size_t col = particle_col_bytes(cap);
     char *b = base + off;
     p.x = (double *)(b + 0 * col);
     p.y = (double *)(b + 1 * col);
@@ -313,6 +317,7 @@ struct pic_ctx {
     bool local_group = false;  // slabs exchanged by pic_step_group (no NCCL)
     bool ghosts_stale = false; // E/B z ghosts need an exchange (after pic_set_fields)
     CUtensorMap eb_map;        // TMA descriptor of the padded E/B array [6][Z][Y][X]
+    CUtensorMap pmap[PIC_MAX_SPECIES][2];   // TMA descriptors of the particle stores A, B ([6][cap + 2])
     int num_sms = 148;
     ncclComm_t comm = nullptr;
     // z slabs: the J ghost / migration exchange of a step runs on st_x while
@@ -522,6 +527,7 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile, int part = 0
         for (int s = 0; s < ctx->cfg.n_species; ++s) {
             if (!ctx->has_particles[s]) continue;
             ts.in[ts.n] = sort_now ? ctx->B[s] : ctx->A[s];
+            ts.pm[ts.n] = ctx->pmap[s][sort_now ? 1 : 0];
             ts.out[ts.n] = ctx->A[s];
             ts.sc_off[ts.n] = ctx->sc_off[s];
             ts.sp[ts.n] = species_dev(ctx, s, jcur);
@@ -758,6 +764,32 @@ int encode_eb_map(pic_ctx *ctx)
     return PIC_OK;
 }
 
+// The particle stores as 2-D tensors [6 components][cap + 2 nodes] (the
+// SoA columns x, y, z, ux, uy, uz at a constant pitch) with a box of
+// [6][kPartBox]: the fused kernel stages a warp's particles with one load.
+int encode_particle_maps(pic_ctx *ctx)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    auto encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    for (int s = 0; s < ctx->cfg.n_species; ++s)
+        for (int k = 0; k < 2; ++k) {
+            const ParticlesDev &P = k ? ctx->B[s] : ctx->A[s];
+            cuuint64_t dims[2] = {(cuuint64_t)ctx->L.cap[s] + 2, 6};
+            cuuint64_t strides[1] = {(cuuint64_t)particle_col_bytes(ctx->L.cap[s])};
+            cuuint32_t box[2] = {(cuuint32_t)kPartBox, 6};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult r = encode(&ctx->pmap[s][k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.x, dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(ctx, PIC_ECUDA, "cuTensorMapEncodeTiled (particles) failed");
+        }
+    return PIC_OK;
+}
+
 int check_device_error(pic_ctx *ctx)
 {
     unsigned h = 0;
@@ -942,7 +974,7 @@ int pic_init(const pic_config *cfg, void *d_workspace, size_t bytes, pic_ctx **o
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    if (ctx->use_tile && encode_eb_map(ctx) != PIC_OK) {
+    if (ctx->use_tile && (encode_eb_map(ctx) != PIC_OK || encode_particle_maps(ctx) != PIC_OK)) {
         delete ctx;
         return PIC_ECUDA;
     }
