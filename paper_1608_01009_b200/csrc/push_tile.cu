@@ -10,9 +10,9 @@
 //      the ghost-padded fields into a bank-conflict-padded shared tile;
 //   2. streams its particles -- the concatenation of the supercell's ranges
 //      [sc_off[s], sc_off[s+1]) of the one or two species of the launch --
-//      through per-thread cp.async (LDGSTS) staging, one particle ahead; the
-//      sort stores them slot-major, so the lanes of a warp sit in distinct
-//      cells;
+//      through shared memory, each warp's 32 with one 2-D TMA tensor load
+//      two iterations ahead (per-warp stages and mbarriers); the sort stores
+//      them slot-major, so the lanes of a warp sit in distinct cells;
 //   3. gathers E/B from the tile, does Boris + move (straight-line code),
 //      stores x, u with coalesced stores, and deposits the Villasenor-Buneman
 //      currents into a deterministic fixed-point J tile with native u32

@@ -1,6 +1,6 @@
 // tma.cuh -- thin inline-PTX wrappers for the sm_100a machinery the fused
 // supercell kernel uses: mbarriers, TMA tensor tile loads
-// (cp.async.bulk.tensor) and per-thread cp.async.
+// (cp.async.bulk.tensor, 2-D particle chunks and 4-D field tiles).
 #pragma once
 #include <cuda.h>
 #include <cstdint>
@@ -86,16 +86,5 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
 // order this thread's earlier generic-proxy shared accesses before later
 // async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// per-thread async 8-byte copy global -> shared (LDGSTS), grouped by commit
-__device__ __forceinline__ void cp_async8(void *dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-
-// wait until at most one committed group is still in flight
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 }  // namespace pic
