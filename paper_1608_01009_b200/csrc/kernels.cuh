@@ -98,9 +98,11 @@ struct TileSpecies {
 // exchanged J ghost planes or leave the slab this step, runtime.cu
 // boundary_layers) and part 2 the layers in between (a no-op when part 1
 // covered them all).
+// zr = [first, end) of the supercell layers launched by part 0 (the occupied
+// ones, runtime.cu push_layers; {0, nsz} for all).
 void launch_push_tile(const CUtensorMap &eb_map, const GridDev &g, const double *EB, double *J,
                       const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb,
-                      cudaStream_t st);
+                      const int zr[2], cudaStream_t st);
 
 // ---- sort.cu : stable counting sort by (supercell, local cell) ----
 struct SortScratch {
@@ -122,6 +124,16 @@ void launch_copy_ids(const uint64_t *src, uint64_t *dst, const int64_t *dev_n, i
 // Sorts the *dev_n particle slots src -> dst (x,y,z,ux,uy,uz,id), dropping
 // dead slots (x == kDeadX); writes the supercell offsets sc_off[0..n_sc]
 // (int64) and the live count back to *dev_n.  Grids are sized for cap.
+// occupied supercell z-layers after a sort (k_occ_range): out = {first, last}
+constexpr int kOccMaxSpecies = 4;   // = PIC_MAX_SPECIES (include/pic.h)
+struct OccRange {
+    const int64_t *sc_off[kOccMaxSpecies];
+    int ns;            // species with particles
+    int64_t per_layer; // supercells per z-layer
+    int nsz;           // supercell layers
+};
+void launch_occ_range(const OccRange &a, int *out, cudaStream_t st);
+
 void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst,
                     int64_t *dev_n, int64_t cap, const SortScratch &s, int64_t *sc_off,
                     unsigned *err, cudaStream_t st, int *launches);

@@ -598,7 +598,8 @@ void launch_u2max(const ParticlesDev &P, int64_t n, unsigned *out, cudaStream_t 
 
 template <int S, int H, bool kGeneral>
 static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
-                        const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb, cudaStream_t st)
+                        const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb,
+                        const int zr[2], cudaStream_t st)
 {
     const size_t smem = TileGeom<S, H>::smem_bytes;
     // one CTA per supercell (empty ones exit at once); only very dense
@@ -617,6 +618,11 @@ static void launch_tile(const CUtensorMap &map, const GridDev &g, const double *
         else { zlo_n = 0; zhi0 = zb; nz_l = g.nsz - 2 * zb; }
     } else if (part == 2) {
         return;   // the boundary part covered every layer
+    } else if (part == 0) {   // only the occupied layers [zr[0], zr[1])
+        zlo_n = 0;
+        zhi0 = zr[0];
+        nz_l = zr[1] - zr[0];
+        if (nz_l <= 0) return;
     }
     const dim3 grid((unsigned)(g.nsx * split), (unsigned)g.nsy, (unsigned)nz_l);
     if (ts.n == 1)
@@ -669,22 +675,23 @@ void configure_tile_kernels()
 
 template <int S, int H>
 static void launch_sh(const CUtensorMap &map, const GridDev &g, const double *EB, double *J, const TileSpecies &ts,
-                      unsigned *err, int64_t mean_per_sc, int part, int zb, cudaStream_t st)
+                      unsigned *err, int64_t mean_per_sc, int part, int zb, const int zr[2], cudaStream_t st)
 {
     if (g.nranks > 1 || g.open_z)
-        launch_tile<S, H, true>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+        launch_tile<S, H, true>(map, g, EB, J, ts, err, mean_per_sc, part, zb, zr, st);
     else
-        launch_tile<S, H, false>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+        launch_tile<S, H, false>(map, g, EB, J, ts, err, mean_per_sc, part, zb, zr, st);
 }
 
 void launch_push_tile(const CUtensorMap &map, const GridDev &g, const double *EB, double *J,
-                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb, cudaStream_t st)
+                      const TileSpecies &ts, unsigned *err, int64_t mean_per_sc, int part, int zb, const int zr[2],
+                      cudaStream_t st)
 {
     if (ts.n == 0) return;
-    if (g.S == 4 && g.H == 1) launch_sh<4, 1>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
-    else if (g.S == 4 && g.H == 2) launch_sh<4, 2>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
-    else if (g.S == 2 && g.H == 1) launch_sh<2, 1>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
-    else if (g.S == 2 && g.H == 2) launch_sh<2, 2>(map, g, EB, J, ts, err, mean_per_sc, part, zb, st);
+    if (g.S == 4 && g.H == 1) launch_sh<4, 1>(map, g, EB, J, ts, err, mean_per_sc, part, zb, zr, st);
+    else if (g.S == 4 && g.H == 2) launch_sh<4, 2>(map, g, EB, J, ts, err, mean_per_sc, part, zb, zr, st);
+    else if (g.S == 2 && g.H == 1) launch_sh<2, 1>(map, g, EB, J, ts, err, mean_per_sc, part, zb, zr, st);
+    else if (g.S == 2 && g.H == 2) launch_sh<2, 2>(map, g, EB, J, ts, err, mean_per_sc, part, zb, zr, st);
 }
 
 }  // namespace pic

@@ -565,6 +565,39 @@ __global__ void k_sc_offsets(const uint32_t *__restrict__ start, int64_t n_sc, i
     if (s == n_sc) *dev_n = (int64_t)start[s * cells_per_sc];
 }
 
+// The supercell z-layers holding particles of any of the given species after
+// a sort: layer z is occupied iff some sc_off[(z+1) L] > sc_off[z L] (L =
+// supercells per layer; z slowest in the supercell order).  out = {first,
+// last} ({nsz, -1} when every layer is empty).  Until the next sort these are
+// exactly the layers whose particle-kernel CTAs have work (particles stay in
+// their sorted supercell's range however far they drift).
+__global__ void __launch_bounds__(256) k_occ_range(OccRange a, int *out)
+{
+    __shared__ int lo, hi;
+    if (threadIdx.x == 0) {
+        lo = a.nsz;
+        hi = -1;
+    }
+    __syncthreads();
+    for (int z = threadIdx.x; z < a.nsz; z += blockDim.x) {
+        bool occ = false;
+        for (int s = 0; s < a.ns; ++s)
+            occ = occ || a.sc_off[s][(int64_t)(z + 1) * a.per_layer] > a.sc_off[s][(int64_t)z * a.per_layer];
+        if (occ) {
+            atomicMin(&lo, z);
+            atomicMax(&hi, z);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {   // `out` may be mapped host memory
+        ((volatile int *)out)[0] = lo;
+        ((volatile int *)out)[1] = hi;
+        __threadfence_system();
+    }
+}
+
+void launch_occ_range(const OccRange &a, int *out, cudaStream_t st) { k_occ_range<<<1, 256, 0, st>>>(a, out); }
+
 void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst,
                     int64_t *dev_n, int64_t cap, const SortScratch &s, int64_t *sc_off,
                     unsigned *err, cudaStream_t st, int *launches)

@@ -323,6 +323,41 @@ def test_two_species_launch_fallback_and_queues(pic, oracle_mod):
     _run_parity(pic, oracle_mod, wl, 25, teacher_forced=False, fields=F6, tol=1e-10)
 
 
+@pytest.mark.parametrize("uz", [3.0, -3.0])
+def test_occupied_layers_follow_a_streaming_slab(pic, oracle_mod, uz):
+    """Particles in 3 of 16 supercell layers streaming at 0.95 c along +z or
+    -z (0.54 cells per step at Courant 0.99, 5.4 per sort interval K = 10):
+    the particle kernel is launched over the occupied layers only
+    (runtime.cu push_layers), so the widened range of each sorting step has
+    to cover every particle, including the slab wrapping through the
+    periodic z end (-z).  40 steps free running against the oracle."""
+    from synth import get_config
+    from synth.configs import electron
+    wl = get_config("C1").with_(species=(electron(2, 0.05),), nz=64, sort_every=10, courant=0.99)
+    rng = np.random.default_rng(31)
+    L = _L(wl)
+    n = wl.nx * wl.ny * 8 * 2
+    P = np.empty((6, n))
+    P[0] = rng.uniform(0.0, L[0], n)
+    P[1] = rng.uniform(0.0, L[1], n)
+    P[2] = rng.uniform(2.0 * wl.dz, 10.0 * wl.dz, n)   # supercell layers 0..2
+    P[3:5] = rng.normal(0.0, 0.05, (2, n))
+    P[5] = uz + rng.normal(0.0, 0.05, n)
+    parts = [(P, np.arange(n, dtype=np.uint64))]
+    orc = _oracle_for(oracle_mod, wl, parts)
+    sim = _sim(pic, wl, counts=[n])
+    _load(sim, parts)
+    for step in range(40):
+        orc.step(1)
+        sim.step(1)
+        errs = list(field_errs(sim.get_fields(), orc.F))
+        gP, gi = sim.get_particles(0)
+        errs += list(compare_state(gP, gi, orc.P[0], orc.ids[0], L))
+        assert max(errs) <= 1e-10, (step, errs)
+    zc = np.floor(orc.P[0][2] / wl.dz)
+    assert (zc < 2).any() or (zc >= 10).any()   # the slab left its starting layers
+
+
 def test_naive_flag_path(pic, oracle_mod):
     from synth import get_config
     wl = get_config("T_small")
