@@ -134,9 +134,12 @@ struct OccRange {
 };
 void launch_occ_range(const OccRange &a, int *out, cudaStream_t st);
 
+// zr (optional): supercell layers [zr[0], zr[1]) known to hold every particle
+// after the sort (runtime.cu push_layers); the per-supercell order kernel
+// runs over those only
 void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst,
                     int64_t *dev_n, int64_t cap, const SortScratch &s, int64_t *sc_off,
-                    unsigned *err, cudaStream_t st, int *launches);
+                    unsigned *err, cudaStream_t st, int *launches, const int *zr = nullptr);
 
 // ---- slab.cu : z-slab exchange helpers ----
 // J ghost planes received from the neighbours are added into the interior

@@ -592,7 +592,7 @@ int phase_push(pic_ctx *ctx, bool sort_now, int jcur, bool profile, int part = 0
         for (int s = 0; s < ctx->cfg.n_species; ++s)
             if (ctx->has_particles[s]) {
                 sort_particles(g, ctx->A[s], ctx->B[s], ctx->dev_n + s, L.cap[s], ctx->sort, ctx->sc_off[s],
-                               ctx->err, ctx->st, &launches);
+                               ctx->err, ctx->st, &launches, ctx->occ_trim && part == 0 ? ctx->push_zr : nullptr);
                 if (ctx->use_tile) {   // the fused kernel never touches ids
                     launch_copy_ids(ctx->B[s].id, ctx->A[s].id, ctx->dev_n + s, L.cap[s], ctx->st);
                     ++launches;

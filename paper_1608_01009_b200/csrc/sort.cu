@@ -398,7 +398,7 @@ __device__ __forceinline__ void warp_order_bucket(const uint32_t *src, uint32_t 
 }
 
 __global__ void __launch_bounds__(kOrderThreads)
-k_order_sc(const uint32_t *__restrict__ start, int cps, uint32_t *perm_tmp, uint32_t *scratch)
+k_order_sc(const uint32_t *__restrict__ start, int cps, uint32_t *perm_tmp, uint32_t *scratch, int64_t sc0)
 {
     extern __shared__ uint32_t sh[];
     uint32_t *cnt = sh;                        // [cps]
@@ -410,7 +410,7 @@ k_order_sc(const uint32_t *__restrict__ start, int cps, uint32_t *perm_tmp, uint
     __shared__ uint32_t maxcnt;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     constexpr int kWarps = kOrderThreads / 32;
-    const int64_t c0 = (int64_t)blockIdx.x * cps;
+    const int64_t c0 = (sc0 + (int64_t)blockIdx.x) * cps;
     const uint32_t base = start[c0];
     const uint32_t n = start[c0 + cps] - base;
     if (n == 0) return;   // uniform per CTA
@@ -600,7 +600,7 @@ void launch_occ_range(const OccRange &a, int *out, cudaStream_t st) { k_occ_rang
 
 void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDev &dst,
                     int64_t *dev_n, int64_t cap, const SortScratch &s, int64_t *sc_off,
-                    unsigned *err, cudaStream_t st, int *launches)
+                    unsigned *err, cudaStream_t st, int *launches, const int *zr)
 {
     const int64_t ncells = (int64_t)g.nx * g.ny * g.nz;
     const int64_t n_sc = (int64_t)g.nsx * g.nsy * g.nsz;
@@ -618,7 +618,11 @@ void sort_particles(const GridDev &g, const ParticlesDev &src, const ParticlesDe
     const int cps = g.S * g.S * g.S;
     const size_t order_smem = sizeof(uint32_t) * (2 * (size_t)cps + 1 + 2 * kOrderCap);
     if (order_smem <= 48 * 1024) {
-        k_order_sc<<<(unsigned)n_sc, kOrderThreads, order_smem, st>>>(s.start, cps, s.perm_tmp, s.perm);
+        // one CTA per supercell of the layers that can hold particles (zr)
+        const int64_t per_layer = (int64_t)g.nsx * g.nsy;
+        const int64_t sc0 = zr ? zr[0] * per_layer : 0, nsc = zr ? (zr[1] - zr[0]) * per_layer : n_sc;
+        if (nsc > 0)
+            k_order_sc<<<(unsigned)nsc, kOrderThreads, order_smem, st>>>(s.start, cps, s.perm_tmp, s.perm, sc0);
     } else {   // very wide supercells: two passes through global memory
         const int64_t threads = ncells * 32;
         k_bucket_order<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(s.start, ncells, s.perm_tmp, s.perm);

@@ -330,7 +330,9 @@ def test_occupied_layers_follow_a_streaming_slab(pic, oracle_mod, uz):
     the particle kernel is launched over the occupied layers only
     (runtime.cu push_layers), so the widened range of each sorting step has
     to cover every particle, including the slab wrapping through the
-    periodic z end (-z).  40 steps free running against the oracle."""
+    periodic z end (-z); the sorts' per-supercell order kernel runs over the
+    same widened layers, so the store's order after every sort must still be
+    the oracle's permutation.  40 steps free running against the oracle."""
     from synth import get_config
     from synth.configs import electron
     wl = get_config("C1").with_(species=(electron(2, 0.05),), nz=64, sort_every=10, courant=0.99)
@@ -347,6 +349,7 @@ def test_occupied_layers_follow_a_streaming_slab(pic, oracle_mod, uz):
     orc = _oracle_for(oracle_mod, wl, parts)
     sim = _sim(pic, wl, counts=[n])
     _load(sim, parts)
+    orc.sort()
     for step in range(40):
         orc.step(1)
         sim.step(1)
@@ -354,6 +357,8 @@ def test_occupied_layers_follow_a_streaming_slab(pic, oracle_mod, uz):
         gP, gi = sim.get_particles(0)
         errs += list(compare_state(gP, gi, orc.P[0], orc.ids[0], L))
         assert max(errs) <= 1e-10, (step, errs)
+        if step % wl.sort_every == 0:   # the sort of this step (its per-supercell order
+            assert np.array_equal(gi, orc.ids[0]), step   # kernel ran over the widened layers)
     zc = np.floor(orc.P[0][2] / wl.dz)
     assert (zc < 2).any() or (zc >= 10).any()   # the slab left its starting layers
 
