@@ -63,9 +63,22 @@ k_b_half(GridDev g, const double *__restrict__ EB, const double *Bin, double *Bo
     }
 }
 
+// does interior plane k (or, at an open face, its z ghost planes) have an
+// image among the padded planes [lo, hi]
+__device__ __forceinline__ bool j_plane_live(const GridDev &g, int k, int lo, int hi)
+{
+    const int kp = k + kGhost;
+    if (hi < lo) return false;
+    if (g.periodic_z_local)
+        return (kp >= lo && kp <= hi) || (kp - g.nz >= lo && kp - g.nz <= hi) ||
+               (kp + g.nz >= lo && kp + g.nz <= hi);
+    const int a = k == 0 ? 0 : kp, b = k == g.nz - 1 ? g.Z - 1 : kp;
+    return a <= hi && b >= lo;
+}
+
 __global__ void __launch_bounds__(256)
 k_e_full(GridDev g, double *__restrict__ EB, const double *__restrict__ Bh, double *__restrict__ Jc,
-         double *__restrict__ Jn, double coefE, double coefJ, StepPrep prep)
+         double *__restrict__ Jn, double coefE, double coefJ, StepPrep prep, JPlanes jl)
 {
     // the next step's J-tile scales (this step's particle kernels are done)
     if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.y) == 0 && (int)threadIdx.x < prep.n_species)
@@ -79,19 +92,26 @@ k_e_full(GridDev g, double *__restrict__ EB, const double *__restrict__ Bh, doub
     const double *Bx = Bh, *By = Bh + cs, *Bz = Bh + 2 * cs;   // B^{n+1/2}
     const int64_t o = pidx(g, i, j, k);
     // fold: the deposit of step n landed on the interior cell and its images
+    // (planes no particle deposited into hold zeros: not read, not cleared)
+    const bool live = j_plane_live(g, k, jl.cur_lo, jl.cur_hi), dirty = j_plane_live(g, k, jl.next_lo, jl.next_hi);
     double jx = 0.0, jy = 0.0, jz = 0.0;
     int nimg = 0;
-    for_images(g, i, j, k, [&](int64_t p) {
-        jx += Jc[p];
-        jy += Jc[cs + p];
-        jz += Jc[2 * cs + p];
-        Jn[p] = 0.0;
-        Jn[cs + p] = 0.0;
-        Jn[2 * cs + p] = 0.0;
-        ++nimg;
-    });
-    if (nimg > 1) {   // the folded J (J^{n+1/2} for pic_get_fields); a cell without
-        Jc[o] = jx;   // images already holds it
+    if (live || dirty)
+        for_images(g, i, j, k, [&](int64_t p) {
+            if (live) {
+                jx += Jc[p];
+                jy += Jc[cs + p];
+                jz += Jc[2 * cs + p];
+            }
+            if (dirty) {
+                Jn[p] = 0.0;
+                Jn[cs + p] = 0.0;
+                Jn[2 * cs + p] = 0.0;
+            }
+            ++nimg;
+        });
+    if (live && nimg > 1) {   // the folded J (J^{n+1/2} for pic_get_fields); a cell
+        Jc[o] = jx;           // without images already holds it
         Jc[cs + o] = jy;
         Jc[2 * cs + o] = jz;
     }
@@ -147,7 +167,7 @@ k_e_full(GridDev g, double *__restrict__ EB, const double *__restrict__ Bh, doub
             Ey[p] = nyK;
         });
     }
-    if (g.nranks == 1) {
+    if (g.nranks == 1 && dirty) {
         // no z images and no slab exchange: clear the z ghost planes of J_next
         // (the deposit spills beyond the faces; those values are dropped)
         const int kz0 = k == 0 ? -kGhost : (k == g.nz - 1 ? g.nz : 0);
@@ -245,11 +265,11 @@ void launch_b_half(const GridDev &g, const double *EB, const double *Bin, double
 }
 
 void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext,
-                   const StepPrep &prep, cudaStream_t st)
+                   const StepPrep &prep, cudaStream_t st, const JPlanes &jl)
 {
     const dim3 bs(32, 8, 1);
     k_e_full<<<field_grid(g, bs), bs, 0, st>>>(g, EB, Bh, Jcur, Jnext, g.c * g.dt,
-                                                4.0 * M_PI * g.dt, prep);
+                                                4.0 * M_PI * g.dt, prep, jl);
 }
 
 void launch_laser_coeffs(const GridDev &g, const double laser[6], int64_t *step, double *out, cudaStream_t st)

@@ -50,8 +50,15 @@ void launch_b_half(const GridDev &g, const double *EB, const double *Bin, double
 // Jcur's interior, stores E to its ghost images and zeroes every image of Jnext.
 // With prep.n_species > 0 its first threads also run the next step's J-tile
 // scale preparation (launch_step_prep's work, after this step's particle kernels).
+// jl = {first, last} padded z planes the particle kernels can have deposited
+// into Jcur (this step, jl[0..1]) and Jnext (the previous step, jl[2..3]);
+// a plane none of whose images lies in its range holds zeros there, so its J
+// is not read (cur) or not cleared (next).  {0, Z - 1}: every plane.
+struct JPlanes {
+    int cur_lo, cur_hi, next_lo, next_hi;
+};
 void launch_e_full(const GridDev &g, double *EB, const double *Bh, double *Jcur, double *Jnext,
-                   const StepPrep &prep, cudaStream_t st);
+                   const StepPrep &prep, cudaStream_t st, const JPlanes &jl);
 // Copies interior values of `ncomp` components to their ghost images.
 void launch_fill_ghosts(const GridDev &g, double *F, int ncomp, cudaStream_t st);
 // NEXT-1 (open z): laser = {e0, omega, ramp, t0, pol_x, pol_y}.  Writes the

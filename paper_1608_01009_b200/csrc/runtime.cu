@@ -330,6 +330,7 @@ struct pic_ctx {
     bool occ_pending = false;
     int occ[2] = {0, -1};      // {first, last} (last < first: no particles)
     int push_zr[2] = {0, 0};   // layers [first, end) the steps being enqueued push
+    int prev_zr[2] = {0, 0};   // ... and the previous step pushed (J zero at init: none)
     CUtensorMap pmap[PIC_MAX_SPECIES][2];   // TMA descriptors of the particle stores A, B ([6][cap + 2])
     int num_sms = 148;
     ncclComm_t comm = nullptr;
@@ -342,7 +343,7 @@ struct pic_ctx {
     std::string last_error;
     // graphs keyed by (sort_now, jcur)
     cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-    int graph_zr[2][2][2] = {};   // the pushed supercell layers each graph was captured with
+    int graph_zr[2][2][4] = {};   // push_zr and prev_zr each graph was captured with
     int graph_launches[2][2] = {{0, 0}, {0, 0}};
     bool graphs_valid = false;
     int64_t launches = 0;
@@ -577,6 +578,33 @@ void push_layers(pic_ctx *ctx, bool sort_now, int zr[2])
     zr[1] = hi + 1;
 }
 
+// The padded J planes [lo, hi] the particle kernel of a step pushing the
+// supercell layers zr = [first, end) can deposit into: the J tiles of those
+// layers, S (z0 - 1) - H - 1 + ... (TileGeom: S + 2H + 3 planes from
+// S z - H - 1), widened for the particles on the global path, which have
+// drifted beyond their tile since the last sort (less than one cell per step,
+// at most K steps; 2 more for the edges of a path); the whole array when
+// that reaches a periodic z end, when there is no sort, or when the layers
+// are not tracked (lo > hi: none).
+void j_planes(const pic_ctx *ctx, const int zr[2], int &lo, int &hi)
+{
+    const GridDev &g = ctx->L.g;
+    lo = 0;
+    hi = g.Z - 1;
+    const int64_t K = ctx->cfg.sort_every;
+    if (!ctx->occ_trim || K <= 0) return;
+    if (zr[1] <= zr[0]) {
+        lo = 1;
+        hi = 0;
+        return;
+    }
+    const int S = g.S, H = g.H, m = (int)std::min<int64_t>(K + 2, g.Z);
+    int a = zr[0] * S - H - 1 + kGhost - m, b = (zr[1] - 1) * S - H - 1 + kGhost + (S + 2 * H + 3) - 1 + m;
+    if (g.periodic_z_local && (a < kGhost || b >= g.nz + kGhost)) return;   // may wrap through z = 0 / L
+    lo = std::max(a, 0);
+    hi = std::min(b, g.Z - 1);
+}
+
 // ---- the phases of one step; each returns the number of kernel launches ----
 // part 0: the whole push; with z slabs part 1 = sort + the boundary supercell
 // layers + the tail kernel + migration headers (everything the step's first
@@ -723,7 +751,10 @@ int phase_fields_e(pic_ctx *ctx, int jcur, bool profile)
         ++launches;
     }
     // + the next step's J-tile scales from this step's bound (parity 1 - jcur)
-    launch_e_full(g, ctx->EB, ctx->Bh, ctx->J[jcur], ctx->J[1 - jcur], make_prep(ctx, 1 - jcur), ctx->st);
+    JPlanes jl;
+    j_planes(ctx, ctx->push_zr, jl.cur_lo, jl.cur_hi);
+    j_planes(ctx, ctx->prev_zr, jl.next_lo, jl.next_hi);
+    launch_e_full(g, ctx->EB, ctx->Bh, ctx->J[jcur], ctx->J[1 - jcur], make_prep(ctx, 1 - jcur), ctx->st, jl);
     return launches + 1;
 }
 
@@ -822,6 +853,8 @@ int build_graph(pic_ctx *ctx, bool sort_now, int jcur)
     ctx->graph_launches[sort_now][jcur] = n;
     ctx->graph_zr[sort_now][jcur][0] = ctx->push_zr[0];
     ctx->graph_zr[sort_now][jcur][1] = ctx->push_zr[1];
+    ctx->graph_zr[sort_now][jcur][2] = ctx->prev_zr[0];
+    ctx->graph_zr[sort_now][jcur][3] = ctx->prev_zr[1];
     return PIC_OK;
 }
 
@@ -1352,8 +1385,9 @@ int pic_step(pic_ctx *ctx, int64_t nsteps)
                 ctx->graphs_valid = true;
             }
             cudaGraphExec_t &ge = ctx->graph[sort_now][jc];
-            if (ge && (ctx->graph_zr[sort_now][jc][0] != ctx->push_zr[0] ||
-                       ctx->graph_zr[sort_now][jc][1] != ctx->push_zr[1])) {   // the occupied layers changed
+            const int *gz = ctx->graph_zr[sort_now][jc];
+            if (ge && (gz[0] != ctx->push_zr[0] || gz[1] != ctx->push_zr[1] || gz[2] != ctx->prev_zr[0] ||
+                       gz[3] != ctx->prev_zr[1])) {   // the occupied layers changed
                 cudaGraphExecDestroy(ge);
                 ge = nullptr;
             }
@@ -1369,6 +1403,8 @@ int pic_step(pic_ctx *ctx, int64_t nsteps)
             ctx->launches += n;
             PIC_CUDA(ctx, cudaGetLastError());
         }
+        ctx->prev_zr[0] = ctx->push_zr[0];
+        ctx->prev_zr[1] = ctx->push_zr[1];
         if (sort_now && ctx->occ_trim) {   // the sort's occupied range is on its way to h_occ
             PIC_CUDA(ctx, cudaEventRecord(ctx->ev_occ, ctx->st));
             ctx->occ_pending = true;
