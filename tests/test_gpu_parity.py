@@ -363,6 +363,52 @@ def test_occupied_layers_follow_a_streaming_slab(pic, oracle_mod, uz):
     assert (zc < 2).any() or (zc >= 10).any()   # the slab left its starting layers
 
 
+def test_reupload_moves_the_occupied_layers(pic, oracle_mod):
+    """A slab in layers 10..12 of 32 runs 7 steps, then the particles are
+    replaced by a slab in layers 22..25 (pic_set_particles between steps, the oracle's
+    state replaced alike): the J planes the last step before the re-upload
+    deposited into must still be cleared (runtime.cu j_planes of the
+    previous step's layers) while the kernel now runs over the new layers.
+    Free running against the oracle on both sides of the re-upload."""
+    from synth import get_config
+    from synth.configs import electron
+    wl = get_config("C1").with_(species=(electron(2, 0.1),), nz=128, sort_every=10)
+    L = _L(wl)
+
+    def slab(z0, z1, seed, id0):
+        rng = np.random.default_rng(seed)
+        n = wl.nx * wl.ny * 8 * 2
+        P = np.empty((6, n))
+        P[0] = rng.uniform(0.0, L[0], n)
+        P[1] = rng.uniform(0.0, L[1], n)
+        P[2] = rng.uniform(z0 * wl.dz, z1 * wl.dz, n)
+        P[3:] = rng.normal(0.0, 0.1, (3, n))
+        return P, np.arange(id0, id0 + n, dtype=np.uint64)
+
+    parts = [slab(40.0, 50.0, 41, 0)]   # far from the periodic ends: no wrap-around widening
+    orc = _oracle_for(oracle_mod, wl, parts)
+    sim = _sim(pic, wl, counts=[parts[0][0].shape[1]])
+    _load(sim, parts)
+
+    def check(step):
+        errs = list(field_errs(sim.get_fields(), orc.F))
+        gP, gi = sim.get_particles(0)
+        errs += list(compare_state(gP, gi, orc.P[0], orc.ids[0], L))
+        assert max(errs) <= 1e-10, (step, errs)
+
+    for step in range(7):
+        orc.step(1)
+        sim.step(1)
+        check(step)
+    P2, i2 = slab(90.0, 100.0, 42, 10 ** 6)
+    orc.P[0], orc.ids[0] = P2.copy(), i2.copy()
+    sim.set_particles(0, P2, i2)
+    for step in range(7, 20):
+        orc.step(1)
+        sim.step(1)
+        check(step)
+
+
 def test_naive_flag_path(pic, oracle_mod):
     from synth import get_config
     wl = get_config("T_small")
