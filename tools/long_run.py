@@ -29,6 +29,8 @@ def main():
     sim = pkg.simulation_from_workload(wl)
     for s, (P, ids) in enumerate(gen_particles(wl)):
         sim.set_particles(s, P, ids)
+    if wl.laser:   # the open laser box starts with the incident wave in the vacuum
+        sim.laser_preload()
     rows = []
     t0 = time.perf_counter()
     done = 0
